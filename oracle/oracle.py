@@ -1,0 +1,281 @@
+"""ctypes view of the CPU oracle (oracle/tfhe_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py.  The product package
+(paper_2407_19871_b200) never imports this module.
+
+Reference anchors (see tfhe_oracle.h for the full list): torus.hpp:19-222 (LWE
+layer), gate_engine.hpp:117-269 (gates), circuits.hpp:187-324 (circuits).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
+
+EXACT, FFT = 0, 1
+GATES = {"and": 0, "or": 1, "xor": 2, "xnor": 3, "nand": 4, "mux": 5, "not": 6, "nor": 7}
+
+
+class Params(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("N", C.c_uint32), ("k", C.c_uint32), ("l", C.c_uint32),
+                ("bgbit", C.c_uint32), ("t", C.c_uint32), ("basebit", C.c_uint32),
+                ("alpha_in", C.c_double), ("alpha_bk", C.c_double)]
+
+
+class KeySet(C.Structure):
+    _fields_ = [("p", Params), ("lwe_key", C.POINTER(C.c_uint8)),
+                ("trlwe_key", C.POINTER(C.c_uint8)), ("bk", C.POINTER(C.c_uint32)),
+                ("ksk", C.POINTER(C.c_uint32)), ("bk_fft", C.POINTER(C.c_double))]
+
+
+class Sampler(C.Structure):
+    _fields_ = [("mt", C.c_uint64 * 312), ("mti", C.c_int), ("sigma", C.c_double)]
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            build()
+        L = C.CDLL(LIB_PATH)
+        u32p = C.POINTER(C.c_uint32)
+        u8p = C.POINTER(C.c_uint8)
+        L.or_keyset_generate.argtypes = [C.POINTER(KeySet), C.POINTER(Params), C.c_uint64]
+        L.or_keyset_free.argtypes = [C.POINTER(KeySet)]
+        L.or_params_default.argtypes = [C.c_int, C.POINTER(Params)]
+        L.or_bk_words.argtypes = [C.POINTER(Params)]
+        L.or_bk_words.restype = C.c_size_t
+        L.or_ksk_words.argtypes = [C.POINTER(Params)]
+        L.or_ksk_words.restype = C.c_size_t
+        L.or_keygen.argtypes = [C.c_uint32, C.c_uint64, u8p]
+        L.or_sampler_init.argtypes = [C.POINTER(Sampler), C.c_uint64, C.c_double]
+        L.or_sampler_uniform.argtypes = [C.POINTER(Sampler)]
+        L.or_sampler_uniform.restype = C.c_uint32
+        L.or_sampler_gaussian.argtypes = [C.POINTER(Sampler)]
+        L.or_sampler_gaussian.restype = C.c_uint32
+        L.or_encrypt_torus.argtypes = [C.c_uint32, u8p, C.c_uint32, C.POINTER(Sampler), u32p]
+        L.or_encrypt_bit.argtypes = [C.c_int, u8p, C.c_uint32, C.POINTER(Sampler), u32p]
+        L.or_phase.argtypes = [u32p, u8p, C.c_uint32]
+        L.or_phase.restype = C.c_uint32
+        L.or_decrypt_bit.argtypes = [u32p, u8p, C.c_uint32]
+        L.or_bootstrap_standin.argtypes = [u32p, u8p, C.c_uint32, C.POINTER(Sampler), u32p]
+        L.or_fft_tables.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.or_fft_forward_i32.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p]
+        L.or_fft_inverse_add.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p]
+        L.or_polymul_exact_add.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.or_decompose.argtypes = [C.POINTER(Params), u32p, C.c_uint32, C.c_void_p]
+        L.or_mod_switch.argtypes = [C.c_uint32, C.c_uint32]
+        L.or_mod_switch.restype = C.c_uint32
+        L.or_blind_rotate_extract.argtypes = [C.POINTER(KeySet), u32p, C.c_uint32, C.c_int, u32p]
+        L.or_blind_rotate_acc.argtypes = [C.POINTER(KeySet), u32p, C.c_uint32, C.c_int,
+                                          C.c_uint32, u32p]
+        L.or_external_product.argtypes = [C.POINTER(KeySet), C.c_uint32, u32p, C.c_int, u32p]
+        L.or_keyswitch.argtypes = [C.POINTER(KeySet), u32p, u32p]
+        L.or_gate.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_int, u32p]
+        L.or_gate_batch.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_uint64,
+                                    C.c_int, C.c_int]
+        _lib = L
+    return _lib
+
+
+def _u32(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _u8(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint8))
+
+
+def params(level: int) -> Params:
+    p = Params()
+    lib().or_params_default(level, C.byref(p))
+    return p
+
+
+def keygen_bits(n: int, seed: int) -> np.ndarray:
+    out = np.zeros(n, np.uint8)
+    lib().or_keygen(n, seed, _u8(out))
+    return out
+
+
+class NoiseSampler:
+    """torus.hpp:119-138 restated in C."""
+
+    def __init__(self, seed: int, sigma: float):
+        self.s = Sampler()
+        lib().or_sampler_init(C.byref(self.s), seed, sigma)
+
+    def uniform(self) -> int:
+        return lib().or_sampler_uniform(C.byref(self.s))
+
+    def gaussian(self) -> int:
+        return lib().or_sampler_gaussian(C.byref(self.s))
+
+
+def encrypt_bit(bit: int, key: np.ndarray, sampler: NoiseSampler) -> np.ndarray:
+    out = np.zeros(len(key) + 1, np.uint32)
+    lib().or_encrypt_bit(int(bit), _u8(key), len(key), C.byref(sampler.s), _u32(out))
+    return out
+
+
+def encrypt_torus(mu: int, key: np.ndarray, sampler: NoiseSampler) -> np.ndarray:
+    out = np.zeros(len(key) + 1, np.uint32)
+    lib().or_encrypt_torus(mu, _u8(key), len(key), C.byref(sampler.s), _u32(out))
+    return out
+
+
+def phase(ct: np.ndarray, key: np.ndarray) -> int:
+    ct = np.ascontiguousarray(ct, np.uint32)
+    return lib().or_phase(_u32(ct), _u8(key), len(key))
+
+
+def decrypt_bit(ct: np.ndarray, key: np.ndarray) -> int:
+    ct = np.ascontiguousarray(ct, np.uint32)
+    return int(lib().or_decrypt_bit(_u32(ct), _u8(key), len(key)))
+
+
+def bootstrap_standin(ct, key, sampler) -> np.ndarray:
+    ct = np.ascontiguousarray(ct, np.uint32)
+    out = np.zeros(len(key) + 1, np.uint32)
+    lib().or_bootstrap_standin(_u32(ct), _u8(key), len(key), C.byref(sampler.s), _u32(out))
+    return out
+
+
+def fft_tables(N: int):
+    W = np.zeros((N // 4, 2))
+    TW = np.zeros((N // 2, 2))
+    UT = np.zeros((N // 2, 2))
+    lib().or_fft_tables(N, W.ctypes.data, TW.ctypes.data, UT.ctypes.data)
+    return W, TW, UT
+
+
+def fft_forward(d: np.ndarray) -> np.ndarray:
+    d = np.ascontiguousarray(d, np.int32)
+    out = np.zeros((len(d) // 2, 2))
+    lib().or_fft_forward_i32(len(d), d.ctypes.data, out.ctypes.data)
+    return out
+
+
+def fft_inverse_add(F: np.ndarray, acc: np.ndarray) -> None:
+    F = np.array(F, np.float64, copy=True)
+    lib().or_fft_inverse_add(len(acc), F.ctypes.data, acc.ctypes.data)
+
+
+def polymul_exact_add(d: np.ndarray, b: np.ndarray, acc: np.ndarray) -> None:
+    d = np.ascontiguousarray(d, np.int32)
+    b = np.ascontiguousarray(b, np.uint32)
+    lib().or_polymul_exact_add(len(acc), d.ctypes.data, b.ctypes.data, acc.ctypes.data)
+
+
+def mod_switch(x: int, N: int) -> int:
+    return lib().or_mod_switch(x, N)
+
+
+class TfheKeys:
+    """Seeded TFHE key set (LWE key, TRLWE key, BK, KSK) -- oracle derivation."""
+
+    def __init__(self, level: int = 128, seed: int = 1, p: Params | None = None):
+        self.ks = KeySet()
+        self.p = p if p is not None else params(level)
+        rc = lib().or_keyset_generate(C.byref(self.ks), C.byref(self.p), seed)
+        if rc:
+            raise RuntimeError(f"or_keyset_generate failed: {rc}")
+        n, N = self.p.n, self.p.N
+        self.n, self.N = n, N
+        self.lwe_key = np.ctypeslib.as_array(self.ks.lwe_key, (n,)).copy()
+        self.trlwe_key = np.ctypeslib.as_array(self.ks.trlwe_key, (N,)).copy()
+        self.bk_words = lib().or_bk_words(C.byref(self.p))
+        self.ksk_words = lib().or_ksk_words(C.byref(self.p))
+
+    def bk(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.ks.bk, (self.bk_words,))
+
+    def ksk(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.ks.ksk, (self.ksk_words,))
+
+    def bk_fft(self) -> np.ndarray:
+        return np.ctypeslib.as_array(self.ks.bk_fft, (self.bk_words,))
+
+    def __del__(self):
+        try:
+            lib().or_keyset_free(C.byref(self.ks))
+        except Exception:
+            pass
+
+    # -- client side -------------------------------------------------------
+    def encrypt(self, bit: int, sampler: NoiseSampler) -> np.ndarray:
+        return encrypt_bit(bit, self.lwe_key, sampler)
+
+    def decrypt(self, ct: np.ndarray) -> int:
+        return decrypt_bit(ct, self.lwe_key)
+
+    def phase(self, ct: np.ndarray) -> int:
+        return phase(ct, self.lwe_key)
+
+    # -- server side (oracle evaluation) -----------------------------------
+    def gate(self, kind: str, a, b=None, c=None, mode: int = FFT) -> np.ndarray:
+        out = np.zeros(self.n + 1, np.uint32)
+        a = np.ascontiguousarray(a, np.uint32)
+        bb = np.ascontiguousarray(b, np.uint32) if b is not None else None
+        cc = np.ascontiguousarray(c, np.uint32) if c is not None else None
+        rc = lib().or_gate(C.byref(self.ks), GATES[kind], _u32(a),
+                           _u32(bb) if bb is not None else None,
+                           _u32(cc) if cc is not None else None, mode, _u32(out))
+        if rc:
+            raise ValueError(f"oracle gate {kind} failed: {rc}")
+        return out
+
+    def gate_batch(self, kind: str, a: np.ndarray, b: np.ndarray, mode: int = FFT,
+                   threads: int = 1) -> np.ndarray:
+        a = np.ascontiguousarray(a, np.uint32)
+        b = np.ascontiguousarray(b, np.uint32)
+        out = np.zeros_like(a)
+        rc = lib().or_gate_batch(C.byref(self.ks), GATES[kind], _u32(a), _u32(b), _u32(out),
+                                 a.shape[0], mode, threads)
+        if rc:
+            raise ValueError(f"oracle gate batch failed: {rc}")
+        return out
+
+    def blind_rotate_extract(self, lwe: np.ndarray, mu: int = 0x20000000,
+                             mode: int = FFT) -> np.ndarray:
+        lwe = np.ascontiguousarray(lwe, np.uint32)
+        out = np.zeros(self.N + 1, np.uint32)
+        lib().or_blind_rotate_extract(C.byref(self.ks), _u32(lwe), mu, mode, _u32(out))
+        return out
+
+    def blind_rotate_acc(self, lwe, mu=0x20000000, mode=FFT, steps=0xFFFFFFFF) -> np.ndarray:
+        lwe = np.ascontiguousarray(lwe, np.uint32)
+        out = np.zeros(2 * self.N, np.uint32)
+        lib().or_blind_rotate_acc(C.byref(self.ks), _u32(lwe), mu, mode, steps, _u32(out))
+        return out
+
+    def external_product(self, i: int, trlwe: np.ndarray, mode: int = FFT) -> np.ndarray:
+        trlwe = np.ascontiguousarray(trlwe, np.uint32)
+        out = np.zeros(2 * self.N, np.uint32)
+        lib().or_external_product(C.byref(self.ks), i, _u32(trlwe), mode, _u32(out))
+        return out
+
+    def keyswitch(self, lweN: np.ndarray) -> np.ndarray:
+        lweN = np.ascontiguousarray(lweN, np.uint32)
+        out = np.zeros(self.n + 1, np.uint32)
+        lib().or_keyswitch(C.byref(self.ks), _u32(lweN), _u32(out))
+        return out
+
+    def decompose(self, x: np.ndarray, level: int) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.uint32)
+        out = np.zeros(self.N, np.int32)
+        lib().or_decompose(C.byref(self.p), _u32(x), level, out.ctypes.data)
+        return out

@@ -1,0 +1,204 @@
+// ref_driver.cpp -- runs the UNMODIFIED reference headers (compiled read-only from
+// /root/reference/proj/include, see oracle/Makefile) and prints golden vectors as
+// JSON.  Test infrastructure only: tests/golden/make_golden.py runs it and commits
+// the output as tests/golden/ref_vectors.json, which pins oracle/tfhe_oracle.c.
+//
+// Also provides the "stand-in" timing mode used by bench.py to report the
+// reference's own refresh-oracle gate rate (gate_engine.hpp:117-123), labelled
+// "functional stand-in, no bootstrapping".
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "locpir/locpir.hpp"
+
+using namespace locpir;
+
+static void put_words(const char* key, const std::vector<uint32_t>& w, bool comma = true)
+{
+    std::printf("\"%s\": [", key);
+    for (size_t i = 0; i < w.size(); i++)
+        std::printf("%s%u", i ? "," : "", w[i]);
+    std::printf("]%s\n", comma ? "," : "");
+}
+
+static std::vector<uint32_t> sample_words(const TlweSample& s)
+{
+    std::vector<uint32_t> w;
+    for (auto t : s.mask)
+        w.push_back(t.raw);
+    w.push_back(s.body.raw);
+    return w;
+}
+
+static int golden()
+{
+    std::printf("{\n");
+    // keygen (torus.hpp:146-154)
+    for (auto [name, p, seed] : {std::tuple{"keygen_sec80_seed11", TlweParams::sec80(), 11ull},
+                                 std::tuple{"keygen_sec128_seed12", TlweParams::sec128(), 12ull},
+                                 std::tuple{"keygen_n630_seed7", TlweParams::custom(630, std::exp2(-15)), 7ull}}) {
+        SecretKey sk = keygen(p, seed);
+        std::vector<uint32_t> bits(sk.bits.begin(), sk.bits.end());
+        put_words(name, bits);
+    }
+    // raw sampler streams (torus.hpp:119-138)
+    {
+        NoiseSampler s(13, TlweParams::sec80().sigma);
+        std::vector<uint32_t> g, u;
+        for (int i = 0; i < 64; i++) {
+            g.push_back(s.gaussian().raw);
+            u.push_back(s.uniform().raw);
+        }
+        put_words("sampler13_sec80_gauss", g);
+        put_words("sampler13_sec80_unif", u);
+        NoiseSampler s2(99, std::exp2(-15));
+        std::vector<uint32_t> g2;
+        for (int i = 0; i < 256; i++)
+            g2.push_back(s2.gaussian().raw);
+        put_words("sampler99_a15_gauss", g2);
+        NoiseSampler s3(5, std::exp2(-25));
+        std::vector<uint32_t> g3;
+        for (int i = 0; i < 256; i++)
+            g3.push_back(s3.gaussian().raw);
+        put_words("sampler5_a25_gauss", g3);
+    }
+    // encryptions (torus.hpp:161-175)
+    {
+        const TlweParams p = TlweParams::sec128();
+        SecretKey sk = keygen(p, 12);
+        NoiseSampler s(14, p.sigma);
+        put_words("enc_sec128_k12_s14_bit1", sample_words(encrypt_bit(true, sk, s)));
+        put_words("enc_sec128_k12_s14_bit0", sample_words(encrypt_bit(false, sk, s)));
+        put_words("enc_sec128_k12_s14_mu0", sample_words(encrypt_torus({0}, sk, s)));
+        TlweSample a = encrypt_bit(true, sk, s);
+        put_words("phase_of_next", {phase(a, sk).raw});
+        put_words("standin_refresh_of_next", sample_words(bootstrap_oracle(a, sk, s)));
+    }
+    {
+        const TlweParams p = TlweParams::custom(630, std::exp2(-15));
+        SecretKey sk = keygen(p, 7);
+        NoiseSampler s(8, p.sigma);
+        std::vector<uint32_t> all;
+        for (int i = 0; i < 4; i++) {
+            auto w = sample_words(encrypt_bit(i & 1, sk, s));
+            all.insert(all.end(), w.begin(), w.end());
+        }
+        put_words("enc_n630_a15_k7_s8_four", all);
+    }
+    // oracle-engine gate outputs (gate_engine.hpp:196-269); deterministic per seed
+    {
+        GateEngine eng = GateEngine::make_tlwe_oracle(keygen(TlweParams::sec80(), 42), 43);
+        std::vector<uint32_t> table;
+        for (int a = 0; a <= 1; a++)
+            for (int b = 0; b <= 1; b++) {
+                CipherBit ca = eng.encrypt(a), cb = eng.encrypt(b);
+                table.push_back(eng.decrypt(eng.hom_and(ca, cb)));
+                table.push_back(eng.decrypt(eng.hom_or(ca, cb)));
+                table.push_back(eng.decrypt(eng.hom_xor(ca, cb)));
+                table.push_back(eng.decrypt(eng.hom_xnor(ca, cb)));
+                table.push_back(eng.decrypt(eng.hom_not(ca)));
+                for (int sl = 0; sl <= 1; sl++) {
+                    CipherBit cs = eng.encrypt(sl);
+                    table.push_back(eng.decrypt(eng.hom_mux(cs, ca, cb)));
+                }
+            }
+        put_words("truth_table_and_or_xor_xnor_not_mux0_mux1", table);
+        auto s = eng.counters().snapshot();
+        put_words("truth_table_counters", {(uint32_t)s.and_gates, (uint32_t)s.or_gates,
+                                           (uint32_t)s.xor_gates, (uint32_t)s.xnor_gates,
+                                           (uint32_t)s.not_gates, (uint32_t)s.mux_gates,
+                                           (uint32_t)s.bootstrap_units()});
+    }
+    // comparator (circuits.hpp:191-216) under the clear engine, l = 6 signed grid
+    {
+        GateEngine eng = GateEngine::make_clear();
+        const FixedPointFormat fmt{4, 2};
+        std::vector<uint32_t> lt, le;
+        for (int64_t a = -32; a < 32; a += 3)
+            for (int64_t b = -32; b < 32; b += 5) {
+                CipherWord ca = encrypt_word(PlainWord::from_integer(a, fmt), eng);
+                CipherWord cb = encrypt_word(PlainWord::from_integer(b, fmt), eng);
+                lt.push_back(eng.decrypt(hom_less(ca, cb, eng)));
+                le.push_back(eng.decrypt(hom_less_equal(ca, cb, eng)));
+            }
+        put_words("cmp_l6_lt_a_m32_s3_b_m32_s5", lt);
+        put_words("cmp_l6_le_a_m32_s3_b_m32_s5", le);
+    }
+    // loc_pir synthetic sweep (bench.hpp:345-384) under the clear engine
+    {
+        std::vector<uint32_t> rows;
+        for (uint32_t N : {1u, 3u, 9u, 16u})
+            for (uint8_t l : {6, 13, 16})
+                for (uint32_t m : {3u, 8u, 9u}) {
+                    if ((int64_t)N * 4 >= (1ll << (l - 1)))
+                        continue;
+                    GateEngine eng = GateEngine::make_clear();
+                    auto c = detail::synthetic_case(N, l, m, eng, nullptr, nullptr);
+                    eng.counters().reset();
+                    auto out = loc_pir(c.x, c.y, c.regions, eng, 1);
+                    auto s = eng.counters().snapshot();
+                    rows.insert(rows.end(),
+                                {N, l, m, (uint32_t)decrypt_service(out, eng), (uint32_t)c.expected,
+                                 (uint32_t)s.bootstrap_units(), (uint32_t)s.xnor_gates,
+                                 (uint32_t)s.mux_gates, (uint32_t)s.and_gates, (uint32_t)s.xor_gates,
+                                 (uint32_t)s.not_gates,
+                                 (uint32_t)predict_gate_units(N, l, m)});
+                }
+        put_words("locpir_synthetic_N_l_m_got_expected_units_xnor_mux_and_xor_not_pred", rows);
+    }
+    // sizes (acceptance.cpp:38-101)
+    {
+        put_words("sample_bytes_sec80_sec128",
+                  {(uint32_t)sample_byte_size(TlweParams::sec80()),
+                   (uint32_t)sample_byte_size(TlweParams::sec128())},
+                  false);
+    }
+    std::printf("}\n");
+    return 0;
+}
+
+// Times the reference refresh-oracle gates (NOT(AND)) on all host threads using the
+// reference partitioner parallel_blocks (parallel.hpp:15-52).
+static int standin(uint64_t gates, unsigned threads)
+{
+    const TlweParams p = TlweParams::sec128();
+    GateEngine eng = GateEngine::make_tlwe_oracle(keygen(p, 1), 2);
+    std::vector<CipherBit> a, b;
+    for (uint64_t i = 0; i < gates; i++) {
+        a.push_back(eng.encrypt(i & 1));
+        b.push_back(eng.encrypt((i >> 1) & 1));
+    }
+    std::vector<CipherBit> out(gates);
+    const uint64_t block = eng.acquire_fork_block();
+    auto t0 = std::chrono::steady_clock::now();
+    parallel_blocks(gates, threads, [&](unsigned w, size_t lo, size_t hi) {
+        GateEngine local = eng.fork((block << 16) | w);
+        for (size_t i = lo; i < hi; i++)
+            out[i] = local.hom_not(local.hom_and(a[i], b[i]));
+    });
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    uint64_t bad = 0;
+    for (uint64_t i = 0; i < gates; i++)
+        bad += eng.decrypt(out[i]) != !((i & 1) && ((i >> 1) & 1));
+    std::printf("{\"gates\": %llu, \"threads\": %u, \"seconds\": %.6f, \"gates_per_s\": %.3f, \"wrong\": %llu}\n",
+                (unsigned long long)gates, threads, secs, gates / secs, (unsigned long long)bad);
+    return bad ? 1 : 0;
+}
+
+int main(int argc, char** argv)
+{
+    if (argc >= 2 && std::strcmp(argv[1], "golden") == 0)
+        return golden();
+    if (argc >= 2 && std::strcmp(argv[1], "standin") == 0) {
+        uint64_t gates = argc >= 3 ? std::strtoull(argv[2], nullptr, 10) : 65536;
+        unsigned threads = argc >= 4 ? (unsigned)std::strtoul(argv[3], nullptr, 10)
+                                     : std::max(1u, std::thread::hardware_concurrency());
+        return standin(gates, threads);
+    }
+    std::fprintf(stderr, "usage: ref_driver golden | standin [gates] [threads]\n");
+    return 2;
+}

@@ -1,0 +1,728 @@
+/*
+ * tfhe_oracle.c -- CPU ORACLE (test infrastructure only; see tfhe_oracle.h).
+ *
+ * Compile with -ffp-contract=off: every floating-point rounding below is
+ * explicit (fma() where a fused multiply-add is meant), because the B200
+ * kernels reproduce this arithmetic bit-for-bit.
+ */
+#include "tfhe_oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------ */
+/* mt19937_64 (the engine behind the reference NoiseSampler, torus.hpp:136)  */
+/* ------------------------------------------------------------------------ */
+#define MT_NN 312
+#define MT_MM 156
+#define MT_MATRIX_A 0xB5026F5AA96619E9ULL
+#define MT_UM 0xFFFFFFFF80000000ULL
+#define MT_LM 0x7FFFFFFFULL
+
+void or_mt64_seed(or_mt64* g, uint64_t seed)
+{
+    g->mt[0] = seed;
+    for (int i = 1; i < MT_NN; i++)
+        g->mt[i] = 6364136223846793005ULL * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+    g->mti = MT_NN;
+}
+
+uint64_t or_mt64_next(or_mt64* g)
+{
+    static const uint64_t mag01[2] = {0ULL, MT_MATRIX_A};
+    uint64_t x;
+    if (g->mti >= MT_NN) {
+        int i;
+        for (i = 0; i < MT_NN - MT_MM; i++) {
+            x = (g->mt[i] & MT_UM) | (g->mt[i + 1] & MT_LM);
+            g->mt[i] = g->mt[i + MT_MM] ^ (x >> 1) ^ mag01[(int)(x & 1ULL)];
+        }
+        for (; i < MT_NN - 1; i++) {
+            x = (g->mt[i] & MT_UM) | (g->mt[i + 1] & MT_LM);
+            g->mt[i] = g->mt[i + (MT_MM - MT_NN)] ^ (x >> 1) ^ mag01[(int)(x & 1ULL)];
+        }
+        x = (g->mt[MT_NN - 1] & MT_UM) | (g->mt[0] & MT_LM);
+        g->mt[MT_NN - 1] = g->mt[MT_MM - 1] ^ (x >> 1) ^ mag01[(int)(x & 1ULL)];
+        g->mti = 0;
+    }
+    x = g->mt[g->mti++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= (x >> 43);
+    return x;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NoiseSampler (torus.hpp:119-138).  The reference constructs a fresh       */
+/* std::normal_distribution<double> per draw (torus.hpp:129), so libstdc++'s */
+/* Marsaglia polar method runs once per draw and its cached second value is  */
+/* discarded.  generate_canonical<double,53> over a 64-bit engine takes one  */
+/* engine output: u / 2^64, clamped below 1.                                 */
+/* ------------------------------------------------------------------------ */
+void or_sampler_init(or_sampler* s, uint64_t seed, double sigma)
+{
+    or_mt64_seed(&s->rng, seed);
+    s->sigma = sigma;
+}
+
+uint32_t or_sampler_uniform(or_sampler* s) { return (uint32_t)or_mt64_next(&s->rng); }
+
+static double canonical(or_mt64* g)
+{
+    double sum = (double)or_mt64_next(g);
+    double ret = sum / 18446744073709551616.0;
+    if (ret >= 1.0)
+        ret = nextafter(1.0, 0.0);
+    return ret;
+}
+
+double or_gaussian_double(or_sampler* s)
+{
+    double x, y, r2;
+    do {
+        x = 2.0 * canonical(&s->rng) - 1.0;
+        y = 2.0 * canonical(&s->rng) - 1.0;
+        r2 = x * x + y * y;
+    } while (r2 > 1.0 || r2 == 0.0);
+    const double mult = sqrt(-2.0 * log(r2) / r2);
+    const double ret = y * mult;
+    return ret * s->sigma + 0.0;
+}
+
+uint32_t or_torus_from_double(double x)
+{
+    double frac = x - floor(x);
+    return (uint32_t)(uint64_t)llround(frac * 4294967296.0);
+}
+
+uint32_t or_sampler_gaussian(or_sampler* s)
+{
+    if (s->sigma == 0.0)
+        return 0;
+    return or_torus_from_double(or_gaussian_double(s));
+}
+
+uint64_t or_child_seed(uint64_t seed, uint64_t lane)
+{
+    uint64_t x = seed + 0x9e3779b97f4a7c15ULL * (lane + 1);
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+/* ------------------------------------------------------------------------ */
+/* LWE layer (torus.hpp:146-222)                                             */
+/* ------------------------------------------------------------------------ */
+void or_keygen(uint32_t n, uint64_t seed, uint8_t* bits)
+{
+    or_mt64 g;
+    or_mt64_seed(&g, seed);
+    for (uint32_t i = 0; i < n; i++)
+        bits[i] = (uint8_t)(or_mt64_next(&g) & 1);
+}
+
+void or_encrypt_torus(uint32_t mu, const uint8_t* key, uint32_t n, or_sampler* s, uint32_t* out)
+{
+    /* torus.hpp:161-170: body = mu + gaussian first, then mask draws */
+    uint32_t body = mu + or_sampler_gaussian(s);
+    for (uint32_t i = 0; i < n; i++) {
+        out[i] = or_sampler_uniform(s);
+        if (key[i])
+            body += out[i];
+    }
+    out[n] = body;
+}
+
+void or_encrypt_bit(int bit, const uint8_t* key, uint32_t n, or_sampler* s, uint32_t* out)
+{
+    or_encrypt_torus(bit ? 0x20000000u : 0xE0000000u, key, n, s, out); /* torus.hpp:52-55 */
+}
+
+uint32_t or_phase(const uint32_t* ct, const uint8_t* key, uint32_t n)
+{
+    uint32_t acc = ct[n];
+    for (uint32_t i = 0; i < n; i++)
+        if (key[i])
+            acc -= ct[i];
+    return acc;
+}
+
+int or_decrypt_bit(const uint32_t* ct, const uint8_t* key, uint32_t n)
+{
+    return or_phase(ct, key, n) <= 0x80000000u; /* torus.hpp:191-194 */
+}
+
+void or_bootstrap_standin(const uint32_t* ct, const uint8_t* key, uint32_t n, or_sampler* s,
+                          uint32_t* out)
+{
+    uint32_t p = or_phase(ct, key, n);
+    int bit = p != 0 && p <= 0x80000000u; /* gate_engine.hpp:117-123 */
+    or_encrypt_bit(bit, key, n, s, out);
+}
+
+/* ------------------------------------------------------------------------ */
+/* TFHE parameters                                                           */
+/* ------------------------------------------------------------------------ */
+void or_params_default(int level, or_params* p)
+{
+    if (level == 80) {
+        or_params q = {500, 1024, 1, 2, 10, 8, 2, 2.44e-5, 7.18e-9};
+        *p = q;
+    } else {
+        or_params q = {630, 1024, 1, 3, 7, 8, 2, 0.0, 0.0};
+        q.alpha_in = ldexp(1.0, -15);
+        q.alpha_bk = ldexp(1.0, -25);
+        *p = q;
+    }
+}
+
+size_t or_bk_words(const or_params* p)
+{
+    return (size_t)p->n * (p->k + 1) * p->l * (p->k + 1) * p->N;
+}
+
+size_t or_ksk_words(const or_params* p)
+{
+    return (size_t)p->N * p->t * ((1u << p->basebit) - 1) * (p->n + 1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Negacyclic FP64 transform.                                                */
+/*   forward: z_j = (a_j + i a_{j+M}) * psi^j, psi = e^{i pi / N}, M = N/2;  */
+/*            radix-2 DIF over M points with W[k] = e^{+2 pi i k / M};       */
+/*            output in bit-reversed order.                                   */
+/*   inverse: radix-2 DIT with conj(W), then * conj(psi^j) / M, round.       */
+/* cmul(x, w) = (fma(xr, wr, -(xi*wi)), fma(xr, wi, xi*wr)).                 */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    double re, im;
+} cplx;
+
+static inline cplx cmul(cplx x, cplx w)
+{
+    cplx r;
+    r.re = fma(x.re, w.re, -(x.im * w.im));
+    r.im = fma(x.re, w.im, x.im * w.re);
+    return r;
+}
+static inline cplx cadd(cplx a, cplx b)
+{
+    cplx r = {a.re + b.re, a.im + b.im};
+    return r;
+}
+static inline cplx csub(cplx a, cplx b)
+{
+    cplx r = {a.re - b.re, a.im - b.im};
+    return r;
+}
+static inline cplx cconj(cplx a)
+{
+    cplx r = {a.re, -a.im};
+    return r;
+}
+
+void or_fft_tables(uint32_t N, double* W, double* TW, double* UT)
+{
+    const uint32_t M = N / 2;
+    const uint32_t Q = M / 4; /* W[k + Q] = i * W[k] exactly */
+    const double pi = 3.14159265358979323846;
+    for (uint32_t k = 0; k < Q; k++) {
+        double re = k == 0 ? 1.0 : cos(2.0 * pi * (double)k / (double)M);
+        double im = k == 0 ? 0.0 : sin(2.0 * pi * (double)k / (double)M);
+        W[2 * k] = re;
+        W[2 * k + 1] = im;
+        W[2 * (k + Q)] = -im;
+        W[2 * (k + Q) + 1] = re;
+    }
+    for (uint32_t j = 0; j < M; j++) {
+        double re = j == 0 ? 1.0 : cos(pi * (double)j / (double)N);
+        double im = j == 0 ? 0.0 : sin(pi * (double)j / (double)N);
+        TW[2 * j] = re;
+        TW[2 * j + 1] = im;
+        UT[2 * j] = re / (double)M;
+        UT[2 * j + 1] = -im / (double)M;
+    }
+}
+
+typedef struct {
+    uint32_t N;
+    cplx* W;
+    cplx* TW;
+    cplx* UT;
+} fft_tab;
+
+static pthread_mutex_t g_tab_lock = PTHREAD_MUTEX_INITIALIZER;
+static fft_tab g_tabs[4];
+static int g_ntabs = 0;
+
+static const fft_tab* get_tab(uint32_t N)
+{
+    pthread_mutex_lock(&g_tab_lock);
+    for (int i = 0; i < g_ntabs; i++)
+        if (g_tabs[i].N == N) {
+            pthread_mutex_unlock(&g_tab_lock);
+            return &g_tabs[i];
+        }
+    fft_tab* t = &g_tabs[g_ntabs++];
+    t->N = N;
+    t->W = (cplx*)malloc(sizeof(cplx) * (N / 4));
+    t->TW = (cplx*)malloc(sizeof(cplx) * (N / 2));
+    t->UT = (cplx*)malloc(sizeof(cplx) * (N / 2));
+    or_fft_tables(N, (double*)t->W, (double*)t->TW, (double*)t->UT);
+    pthread_mutex_unlock(&g_tab_lock);
+    return t;
+}
+
+static void dif_forward(uint32_t M, cplx* z, const cplx* W)
+{
+    uint32_t s = 0;
+    for (uint32_t h = M >> 1; h >= 1; h >>= 1, s++) {
+        for (uint32_t b = 0; b < M; b += 2 * h)
+            for (uint32_t j = 0; j < h; j++) {
+                cplx u = z[b + j], v = z[b + j + h];
+                z[b + j] = cadd(u, v);
+                z[b + j + h] = cmul(csub(u, v), W[j << s]);
+            }
+    }
+}
+
+static void dit_inverse(uint32_t M, cplx* z, const cplx* W)
+{
+    uint32_t logM = 0;
+    while ((1u << logM) < M)
+        logM++;
+    for (int s = (int)logM - 1; s >= 0; s--) {
+        uint32_t h = M >> (s + 1);
+        for (uint32_t b = 0; b < M; b += 2 * h)
+            for (uint32_t j = 0; j < h; j++) {
+                cplx u = z[b + j];
+                cplx v = cmul(z[b + j + h], cconj(W[j << s]));
+                z[b + j] = cadd(u, v);
+                z[b + j + h] = csub(u, v);
+            }
+    }
+}
+
+void or_fft_forward_i32(uint32_t N, const int32_t* in, double* out)
+{
+    const fft_tab* t = get_tab(N);
+    const uint32_t M = N / 2;
+    cplx* z = (cplx*)out;
+    for (uint32_t j = 0; j < M; j++) {
+        cplx a = {(double)in[j], (double)in[j + M]};
+        z[j] = cmul(a, t->TW[j]);
+    }
+    dif_forward(M, z, t->W);
+}
+
+void or_fft_inverse_add(uint32_t N, double* in, uint32_t* acc)
+{
+    const fft_tab* t = get_tab(N);
+    const uint32_t M = N / 2;
+    cplx* z = (cplx*)in;
+    dit_inverse(M, z, t->W);
+    for (uint32_t j = 0; j < M; j++) {
+        cplx w = cmul(z[j], t->UT[j]);
+        acc[j] += (uint32_t)(uint64_t)llrint(w.re);
+        acc[j + M] += (uint32_t)(uint64_t)llrint(w.im);
+    }
+}
+
+void or_polymul_exact_add(uint32_t N, const int32_t* d, const uint32_t* b, uint32_t* acc)
+{
+    for (uint32_t m = 0; m < N; m++) {
+        const uint32_t dm = (uint32_t)d[m];
+        if (dm == 0)
+            continue;
+        /* X^m * b : coefficient j gets b[j-m] (j>=m) or -b[j-m+N] */
+        for (uint32_t j = 0; j < m; j++)
+            acc[j] -= dm * b[j - m + N];
+        for (uint32_t j = m; j < N; j++)
+            acc[j] += dm * b[j - m];
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Gadget decomposition: signed digits with the rounding offset               */
+/* (x' = x + sum_p Bg/2 * 2^(32-p*Bgbit) + 2^(31 - l*Bgbit)).                 */
+/* ------------------------------------------------------------------------ */
+static uint32_t decomp_offset(const or_params* p)
+{
+    uint32_t off = 0;
+    const uint32_t half = 1u << (p->bgbit - 1);
+    for (uint32_t q = 1; q <= p->l; q++)
+        off += half << (32 - q * p->bgbit);
+    off += 1u << (31 - p->l * p->bgbit);
+    return off;
+}
+
+void or_decompose(const or_params* p, const uint32_t* x, uint32_t level, int32_t* digits)
+{
+    const uint32_t off = decomp_offset(p);
+    const uint32_t shift = 32 - (level + 1) * p->bgbit;
+    const uint32_t mask = (1u << p->bgbit) - 1;
+    const int32_t half = 1 << (p->bgbit - 1);
+    for (uint32_t j = 0; j < p->N; j++)
+        digits[j] = (int32_t)(((x[j] + off) >> shift) & mask) - half;
+}
+
+uint32_t or_mod_switch(uint32_t x, uint32_t N)
+{
+    uint32_t logN2 = 0;
+    while ((1u << logN2) < 2 * N)
+        logN2++;
+    const uint32_t sh = 32 - logN2;
+    return (uint32_t)(x + (1u << (sh - 1))) >> sh;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Key set                                                                   */
+/* ------------------------------------------------------------------------ */
+static void negacyclic_mul_binary_add(uint32_t N, const uint32_t* a, const uint8_t* z,
+                                      uint32_t* acc)
+{
+    for (uint32_t m = 0; m < N; m++) {
+        if (!z[m])
+            continue;
+        for (uint32_t j = 0; j < m; j++)
+            acc[j] -= a[j - m + N];
+        for (uint32_t j = m; j < N; j++)
+            acc[j] += a[j - m];
+    }
+}
+
+int or_keyset_generate(or_keyset* ks, const or_params* p, uint64_t seed)
+{
+    if (p->k != 1 || p->N < 16 || (p->N & (p->N - 1)))
+        return -1;
+    memset(ks, 0, sizeof(*ks));
+    ks->p = *p;
+    const uint32_t n = p->n, N = p->N, rows = (p->k + 1) * p->l;
+    const uint32_t base = 1u << p->basebit;
+    ks->lwe_key = (uint8_t*)malloc(n);
+    ks->trlwe_key = (uint8_t*)malloc(N);
+    ks->bk = (uint32_t*)malloc(sizeof(uint32_t) * or_bk_words(p));
+    ks->ksk = (uint32_t*)malloc(sizeof(uint32_t) * or_ksk_words(p));
+    ks->bk_fft = (double*)malloc(sizeof(double) * or_bk_words(p));
+    if (!ks->lwe_key || !ks->trlwe_key || !ks->bk || !ks->ksk || !ks->bk_fft)
+        return -2;
+
+    /* LWE key: the reference keygen (torus.hpp:146-154) */
+    or_keygen(n, seed, ks->lwe_key);
+    /* TRLWE key: N binary coefficients from an independent lane */
+    {
+        or_mt64 g;
+        or_mt64_seed(&g, or_child_seed(seed, 1));
+        for (uint32_t j = 0; j < N; j++)
+            ks->trlwe_key[j] = (uint8_t)(or_mt64_next(&g) & 1);
+    }
+    /* BK: n TRGSW encryptions of s_i; row (c, q) = TRLWE_z(0) + s_i * 2^(32-(q+1)Bgbit)
+     * on component c.  Draw order per row: N uniform mask coefficients, then N
+     * Gaussian noise coefficients. */
+    {
+        or_sampler s;
+        or_sampler_init(&s, or_child_seed(seed, 2), p->alpha_bk);
+        for (uint32_t i = 0; i < n; i++)
+            for (uint32_t r = 0; r < rows; r++) {
+                uint32_t* A = ks->bk + (((size_t)i * rows + r) * 2 + 0) * N;
+                uint32_t* B = ks->bk + (((size_t)i * rows + r) * 2 + 1) * N;
+                for (uint32_t j = 0; j < N; j++)
+                    A[j] = or_sampler_uniform(&s);
+                for (uint32_t j = 0; j < N; j++)
+                    B[j] = or_sampler_gaussian(&s);
+                negacyclic_mul_binary_add(N, A, ks->trlwe_key, B);
+                const uint32_t c = r / p->l, q = r % p->l;
+                const uint32_t h = 1u << (32 - (q + 1) * p->bgbit);
+                if (ks->lwe_key[i]) {
+                    if (c == 0)
+                        A[0] += h;
+                    else
+                        B[0] += h;
+                }
+            }
+    }
+    /* KSK[i][j][h-1] = LWE_s(h * z_i * 2^(32-(j+1)basebit)) with the reference
+     * encrypt_torus (torus.hpp:161-170). */
+    {
+        or_sampler s;
+        or_sampler_init(&s, or_child_seed(seed, 3), p->alpha_in);
+        uint32_t* out = ks->ksk;
+        for (uint32_t i = 0; i < N; i++)
+            for (uint32_t j = 0; j < p->t; j++)
+                for (uint32_t h = 1; h < base; h++) {
+                    const uint32_t mu = (h * ks->trlwe_key[i]) << (32 - (j + 1) * p->basebit);
+                    or_encrypt_torus(mu, ks->lwe_key, n, &s, out);
+                    out += n + 1;
+                }
+    }
+    /* frequency-domain BK */
+    {
+        int32_t* tmp = (int32_t*)malloc(sizeof(int32_t) * N);
+        const size_t polys = (size_t)n * rows * 2;
+        for (size_t q = 0; q < polys; q++) {
+            for (uint32_t j = 0; j < N; j++)
+                tmp[j] = (int32_t)ks->bk[q * N + j];
+            or_fft_forward_i32(N, tmp, ks->bk_fft + q * N);
+        }
+        free(tmp);
+    }
+    return 0;
+}
+
+void or_keyset_free(or_keyset* ks)
+{
+    free(ks->lwe_key);
+    free(ks->trlwe_key);
+    free(ks->bk);
+    free(ks->ksk);
+    free(ks->bk_fft);
+    memset(ks, 0, sizeof(*ks));
+}
+
+/* ------------------------------------------------------------------------ */
+/* Bootstrapping                                                             */
+/* ------------------------------------------------------------------------ */
+/* out = X^e * in, e in [0, 2N) */
+static void poly_mul_xai(uint32_t N, uint32_t e, const uint32_t* in, uint32_t* out)
+{
+    if (e < N) {
+        for (uint32_t j = 0; j < e; j++)
+            out[j] = 0u - in[j - e + N];
+        for (uint32_t j = e; j < N; j++)
+            out[j] = in[j - e];
+    } else {
+        const uint32_t f = e - N;
+        for (uint32_t j = 0; j < f; j++)
+            out[j] = in[j - f + N];
+        for (uint32_t j = f; j < N; j++)
+            out[j] = 0u - in[j - f];
+    }
+}
+
+int or_external_product(const or_keyset* ks, uint32_t i, const uint32_t* trlwe, int mode,
+                        uint32_t* out)
+{
+    const or_params* p = &ks->p;
+    const uint32_t N = p->N, M = N / 2, rows = (p->k + 1) * p->l;
+    int32_t* dig = (int32_t*)malloc(sizeof(int32_t) * N);
+    memset(out, 0, sizeof(uint32_t) * 2 * N);
+    if (mode == ORACLE_EXACT) {
+        for (uint32_t c = 0; c < 2; c++)
+            for (uint32_t q = 0; q < p->l; q++) {
+                or_decompose(p, trlwe + c * N, q, dig);
+                const uint32_t r = c * p->l + q;
+                for (uint32_t comp = 0; comp < 2; comp++)
+                    or_polymul_exact_add(N, dig, ks->bk + (((size_t)i * rows + r) * 2 + comp) * N,
+                                         out + comp * N);
+            }
+    } else {
+        cplx* F = (cplx*)malloc(sizeof(cplx) * M);
+        cplx* acc = (cplx*)calloc(2 * M, sizeof(cplx));
+        for (uint32_t c = 0; c < 2; c++)
+            for (uint32_t q = 0; q < p->l; q++) {
+                or_decompose(p, trlwe + c * N, q, dig);
+                or_fft_forward_i32(N, dig, (double*)F);
+                const uint32_t r = c * p->l + q;
+                for (uint32_t comp = 0; comp < 2; comp++) {
+                    const cplx* B =
+                        (const cplx*)(ks->bk_fft + (((size_t)i * rows + r) * 2 + comp) * N);
+                    cplx* a = acc + comp * M;
+                    for (uint32_t f = 0; f < M; f++) {
+                        double re = fma(F[f].re, B[f].re, a[f].re);
+                        re = fma(-F[f].im, B[f].im, re);
+                        double im = fma(F[f].re, B[f].im, a[f].im);
+                        im = fma(F[f].im, B[f].re, im);
+                        a[f].re = re;
+                        a[f].im = im;
+                    }
+                }
+            }
+        for (uint32_t comp = 0; comp < 2; comp++)
+            or_fft_inverse_add(N, (double*)(acc + comp * M), out + comp * N);
+        free(F);
+        free(acc);
+    }
+    free(dig);
+    return 0;
+}
+
+int or_blind_rotate_acc(const or_keyset* ks, const uint32_t* lwe_in, uint32_t mu, int mode,
+                        uint32_t steps, uint32_t* acc)
+{
+    const or_params* p = &ks->p;
+    const uint32_t n = p->n, N = p->N;
+    uint32_t* v = (uint32_t*)malloc(sizeof(uint32_t) * N);
+    uint32_t* tmp = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+    uint32_t* ext = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+    for (uint32_t j = 0; j < N; j++)
+        v[j] = mu;
+    const uint32_t bbar = or_mod_switch(lwe_in[n], N);
+    memset(acc, 0, sizeof(uint32_t) * N);
+    poly_mul_xai(N, (2 * N - bbar) % (2 * N), v, acc + N);
+    for (uint32_t i = 0; i < n && i < steps; i++) {
+        const uint32_t a = or_mod_switch(lwe_in[i], N);
+        if (a == 0)
+            continue;
+        for (uint32_t c = 0; c < 2; c++) {
+            poly_mul_xai(N, a, acc + c * N, tmp + c * N);
+            for (uint32_t j = 0; j < N; j++)
+                tmp[c * N + j] -= acc[c * N + j];
+        }
+        or_external_product(ks, i, tmp, mode, ext);
+        for (uint32_t j = 0; j < 2 * N; j++)
+            acc[j] += ext[j];
+    }
+    free(v);
+    free(tmp);
+    free(ext);
+    return 0;
+}
+
+int or_blind_rotate_extract(const or_keyset* ks, const uint32_t* lwe_in, uint32_t mu, int mode,
+                            uint32_t* out_N)
+{
+    const uint32_t N = ks->p.N;
+    uint32_t* acc = (uint32_t*)malloc(sizeof(uint32_t) * 2 * N);
+    or_blind_rotate_acc(ks, lwe_in, mu, mode, 0xFFFFFFFFu, acc);
+    /* sample extraction at index 0 */
+    out_N[0] = acc[0];
+    for (uint32_t j = 1; j < N; j++)
+        out_N[j] = 0u - acc[N - j];
+    out_N[N] = acc[N];
+    free(acc);
+    return 0;
+}
+
+void or_keyswitch(const or_keyset* ks, const uint32_t* in_N, uint32_t* out_n)
+{
+    const or_params* p = &ks->p;
+    const uint32_t n = p->n, N = p->N, base = 1u << p->basebit;
+    const uint32_t prec = 1u << (32 - (1 + p->basebit * p->t));
+    const uint32_t mask = base - 1;
+    memset(out_n, 0, sizeof(uint32_t) * n);
+    out_n[n] = in_N[N];
+    for (uint32_t i = 0; i < N; i++) {
+        const uint32_t abar = in_N[i] + prec;
+        for (uint32_t j = 0; j < p->t; j++) {
+            const uint32_t d = (abar >> (32 - (j + 1) * p->basebit)) & mask;
+            if (!d)
+                continue;
+            const uint32_t* row = ks->ksk + (((size_t)i * p->t + j) * (base - 1) + (d - 1)) * (n + 1);
+            for (uint32_t q = 0; q <= n; q++)
+                out_n[q] -= row[q];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Gates                                                                     */
+/* ------------------------------------------------------------------------ */
+static void lin2(uint32_t n, uint32_t off, int32_t ca, const uint32_t* a, int32_t cb,
+                 const uint32_t* b, uint32_t* out)
+{
+    for (uint32_t q = 0; q <= n; q++)
+        out[q] = (uint32_t)ca * a[q] + (uint32_t)cb * b[q];
+    out[n] += off;
+}
+
+int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
+            const uint32_t* c, int mode, uint32_t* out)
+{
+    const uint32_t n = ks->p.n, N = ks->p.N;
+    const uint32_t MU = 0x20000000u;
+    uint32_t* comb = (uint32_t*)malloc(sizeof(uint32_t) * (n + 1));
+    uint32_t* ext = (uint32_t*)malloc(sizeof(uint32_t) * (N + 1));
+    int rc = 0;
+    switch (kind) {
+    case OR_GATE_AND: lin2(n, 0xE0000000u, 1, a, 1, b, comb); break;
+    case OR_GATE_OR: lin2(n, 0x20000000u, 1, a, 1, b, comb); break;
+    case OR_GATE_XOR: lin2(n, 0x40000000u, 2, a, 2, b, comb); break;
+    case OR_GATE_XNOR: lin2(n, 0xC0000000u, -2, a, -2, b, comb); break;
+    case OR_GATE_NAND: lin2(n, 0x20000000u, -1, a, -1, b, comb); break;
+    case OR_GATE_NOR: lin2(n, 0xE0000000u, -1, a, -1, b, comb); break;
+    case OR_GATE_NOT:
+        for (uint32_t q = 0; q <= n; q++)
+            out[q] = 0u - a[q];
+        goto done;
+    case OR_GATE_MUX: {
+        /* TFHE MUX: u1 = BR(-1/8 + s + a), u2 = BR(-1/8 - s + b), out = KS(u1 + u2 + 1/8) */
+        uint32_t* ext2 = (uint32_t*)malloc(sizeof(uint32_t) * (N + 1));
+        lin2(n, 0xE0000000u, 1, a, 1, b, comb);
+        or_blind_rotate_extract(ks, comb, MU, mode, ext);
+        lin2(n, 0xE0000000u, -1, a, 1, c, comb);
+        or_blind_rotate_extract(ks, comb, MU, mode, ext2);
+        for (uint32_t q = 0; q <= N; q++)
+            ext[q] += ext2[q];
+        ext[N] += 0x20000000u;
+        or_keyswitch(ks, ext, out);
+        free(ext2);
+        goto done;
+    }
+    default: rc = -1; goto done;
+    }
+    or_blind_rotate_extract(ks, comb, MU, mode, ext);
+    or_keyswitch(ks, ext, out);
+done:
+    free(comb);
+    free(ext);
+    return rc;
+}
+
+typedef struct {
+    const or_keyset* ks;
+    int kind, mode;
+    const uint32_t *a, *b;
+    uint32_t* out;
+    uint64_t lo, hi;
+    int rc;
+} batch_job;
+
+static void* batch_worker(void* arg)
+{
+    batch_job* j = (batch_job*)arg;
+    const size_t w = j->ks->p.n + 1;
+    for (uint64_t g = j->lo; g < j->hi; g++) {
+        int rc = or_gate(j->ks, j->kind, j->a + g * w, j->b ? j->b + g * w : NULL, NULL, j->mode,
+                         j->out + g * w);
+        if (rc)
+            j->rc = rc;
+    }
+    return NULL;
+}
+
+int or_gate_batch(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
+                  uint32_t* out, uint64_t count, int mode, int threads)
+{
+    if (threads < 1)
+        threads = 1;
+    if ((uint64_t)threads > count)
+        threads = count ? (int)count : 1;
+    batch_job* jobs = (batch_job*)calloc(threads, sizeof(batch_job));
+    pthread_t* tid = (pthread_t*)calloc(threads, sizeof(pthread_t));
+    const uint64_t chunk = (count + threads - 1) / threads; /* parallel.hpp:26-34 */
+    for (int w = 0; w < threads; w++) {
+        jobs[w].ks = ks;
+        jobs[w].kind = kind;
+        jobs[w].mode = mode;
+        jobs[w].a = a;
+        jobs[w].b = b;
+        jobs[w].out = out;
+        jobs[w].lo = (uint64_t)w * chunk < count ? (uint64_t)w * chunk : count;
+        jobs[w].hi = jobs[w].lo + chunk < count ? jobs[w].lo + chunk : count;
+    }
+    for (int w = 1; w < threads; w++)
+        pthread_create(&tid[w], NULL, batch_worker, &jobs[w]);
+    batch_worker(&jobs[0]);
+    int rc = jobs[0].rc;
+    for (int w = 1; w < threads; w++) {
+        pthread_join(tid[w], NULL);
+        if (jobs[w].rc)
+            rc = jobs[w].rc;
+    }
+    free(jobs);
+    free(tid);
+    return rc;
+}
