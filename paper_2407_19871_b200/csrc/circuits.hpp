@@ -1,0 +1,115 @@
+// circuits.hpp -- LocPIR circuits emitted as gate programs (host C++, no CUDA).
+//
+// Gate-for-gate restatement of the reference circuits (circuits.hpp:187-324) over
+// pool slots, so gate counts are exactly N(12l + 2m + 3) units per query
+// (bench.hpp:35-43).  The scheduler (program.hpp) batches every independent gate
+// of all queries and regions into one level.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "../../include/locpir_b200.h"
+
+namespace lpb {
+
+struct Emitter {
+    std::vector<locpir_b200_gate_op>* ops;
+    uint64_t next;  // next free scratch slot
+    uint32_t fresh() { return (uint32_t)next++; }
+    uint32_t gate(uint32_t kind, uint32_t a, uint32_t b = 0xFFFFFFFFu, uint32_t c = 0xFFFFFFFFu,
+                  uint32_t out = 0xFFFFFFFFu)
+    {
+        if (out == 0xFFFFFFFFu)
+            out = fresh();
+        ops->push_back({kind, a, b, c, out});
+        return out;
+    }
+};
+
+// hom_less (circuits.hpp:191-209): flip both sign bits (free NOTs), then
+// t0 = 0; t1 = XNOR(a_i, b_i); t0 = MUX(t1, t0, b_i) for i = 0..l-1.
+inline uint32_t emit_less(Emitter& e, const uint32_t* a, const uint32_t* b, uint32_t l)
+{
+    const uint32_t a_sign = e.gate(LOCPIR_B200_NOT, a[l - 1]);
+    const uint32_t b_sign = e.gate(LOCPIR_B200_NOT, b[l - 1]);
+    uint32_t t0 = e.gate(LOCPIR_B200_CONST, 0);
+    for (uint32_t i = 0; i < l; i++) {
+        const uint32_t ai = (i + 1 == l) ? a_sign : a[i];
+        const uint32_t bi = (i + 1 == l) ? b_sign : b[i];
+        const uint32_t t1 = e.gate(LOCPIR_B200_XNOR, ai, bi);
+        t0 = e.gate(LOCPIR_B200_MUX, t1, t0, bi);
+    }
+    return t0;
+}
+
+// hom_less_equal (circuits.hpp:212-216): NOT(b < a).
+inline uint32_t emit_less_equal(Emitter& e, const uint32_t* a, const uint32_t* b, uint32_t l)
+{
+    return e.gate(LOCPIR_B200_NOT, emit_less(e, b, a, l));
+}
+
+inline uint64_t loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
+{
+    // per region: 4 comparators x (2 NOT + 1 CONST + 2l) + 2 NOT + 3 AND + m AND;
+    // per query and bit column: 1 CONST + (R - 1) XOR
+    const uint64_t per_region = 4ull * (3 + 2ull * l) + 2 + 3 + m;
+    const uint64_t per_query = (uint64_t)R * per_region + (uint64_t)m * (1 + R);
+    return (uint64_t)Q * per_query;
+}
+
+// loc_pir (circuits.hpp:276-324) for Q queries.  xor_tree = 0 keeps the
+// reference's N-long chain per bit column (circuits.hpp:257-261); 1 uses a
+// balanced tree of N-1 XORs plus one XOR with Enc(0): still N*m XOR units.
+inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
+                         uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
+                         const uint32_t* bnd, const uint32_t* svc, const uint32_t* out,
+                         uint64_t scratch_first, int xor_tree)
+{
+    Emitter e{&ops, scratch_first};
+    std::vector<uint32_t> masked((size_t)R * m);
+    for (uint32_t q = 0; q < Q; q++) {
+        const uint32_t* x = xs + (size_t)q * l;
+        const uint32_t* y = ys + (size_t)q * l;
+        for (uint32_t r = 0; r < R; r++) {
+            const uint32_t* x1 = bnd + ((size_t)r * 4 + 0) * l;
+            const uint32_t* x2 = bnd + ((size_t)r * 4 + 1) * l;
+            const uint32_t* y1 = bnd + ((size_t)r * 4 + 2) * l;
+            const uint32_t* y2 = bnd + ((size_t)r * 4 + 3) * l;
+            const uint32_t x_l = emit_less_equal(e, x1, x, l);
+            const uint32_t x_r = emit_less(e, x, x2, l);
+            const uint32_t y_l = emit_less_equal(e, y1, y, l);
+            const uint32_t y_r = emit_less(e, y, y2, l);
+            const uint32_t v1 = e.gate(LOCPIR_B200_AND, x_l, x_r);
+            const uint32_t v2 = e.gate(LOCPIR_B200_AND, y_l, y_r);
+            const uint32_t f = e.gate(LOCPIR_B200_AND, v1, v2);
+            for (uint32_t j = 0; j < m; j++)  // mask_service (circuits.hpp:219-227)
+                masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc[(size_t)r * m + j]);
+        }
+        // xor_sum_services (circuits.hpp:240-269)
+        for (uint32_t j = 0; j < m; j++) {
+            const uint32_t dst = out[(size_t)q * m + j];
+            const uint32_t zero = e.gate(LOCPIR_B200_CONST, 0);
+            if (!xor_tree) {
+                uint32_t acc = zero;
+                for (uint32_t r = 0; r < R; r++)
+                    acc = e.gate(LOCPIR_B200_XOR, acc, masked[(size_t)r * m + j], 0xFFFFFFFFu,
+                                 r + 1 == R ? dst : 0xFFFFFFFFu);
+            } else {
+                std::vector<uint32_t> lvl(R);
+                for (uint32_t r = 0; r < R; r++)
+                    lvl[r] = masked[(size_t)r * m + j];
+                while (lvl.size() > 1) {
+                    std::vector<uint32_t> nxt;
+                    for (size_t i = 0; i + 1 < lvl.size(); i += 2)
+                        nxt.push_back(e.gate(LOCPIR_B200_XOR, lvl[i], lvl[i + 1]));
+                    if (lvl.size() & 1)
+                        nxt.push_back(lvl.back());
+                    lvl.swap(nxt);
+                }
+                e.gate(LOCPIR_B200_XOR, zero, lvl[0], 0xFFFFFFFFu, dst);
+            }
+        }
+    }
+}
+
+}  // namespace lpb

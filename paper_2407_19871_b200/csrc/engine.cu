@@ -1,0 +1,758 @@
+// engine.cu -- device context, ciphertext pool, level-batched execution and the
+// C ABI (include/locpir_b200.h).  Host C++ around the sm_100a kernels of
+// kernels.cuh; no CPU fallback exists: every gate runs on the GPU.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/locpir_b200.h"
+#include "circuits.hpp"
+#include "kernels.cuh"
+#include "program.hpp"
+
+using namespace lpb;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess)                                                             \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));              \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t want, cudaStream_t s, bool keep)
+    {
+        if (want <= n)
+            return;
+        size_t cap = std::max(want, n + n / 2);
+        T* q = nullptr;
+        CK(cudaMalloc(&q, cap * sizeof(T)));
+        if (keep && p && n)
+            CK(cudaMemcpyAsync(q, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+        if (p) {
+            CK(cudaStreamSynchronize(s));
+            CK(cudaFree(p));
+        }
+        p = q;
+        n = cap;
+    }
+    ~DevBuf()
+    {
+        if (p)
+            cudaFree(p);
+    }
+};
+
+template <class T>
+struct PinnedBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t want)
+    {
+        if (want <= n)
+            return;
+        if (p)
+            cudaFreeHost(p);
+        n = std::max(want, n * 2);
+        if (cudaMallocHost(&p, n * sizeof(T)) != cudaSuccess) {
+            p = nullptr;
+            n = 0;
+            throw CudaError("cudaMallocHost failed");
+        }
+    }
+    ~PinnedBuf()
+    {
+        if (p)
+            cudaFreeHost(p);
+    }
+};
+
+struct Timer {
+    std::vector<cudaEvent_t> ev[3];  // start/stop pairs per kernel class
+    double ms[3] = {0, 0, 0};
+    uint64_t launches[3] = {0, 0, 0};
+};
+
+}  // namespace
+
+struct locpir_b200_ctx {
+    locpir_b200_params p{};
+    DevParams dp{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+    DevBuf<double2> W, TW, UT, bkf;
+    DevBuf<uint32_t> ksk;
+    bool have_keys = false;
+    DevBuf<uint32_t> pool_n, pool_N;
+    uint64_t pool_slots = 0, scratch_slots = 0;
+    DevBuf<BrItem> d_br;
+    DevBuf<KsItem> d_ks;
+    DevBuf<LinItem> d_lin;
+    PinnedBuf<BrItem> h_br;
+    PinnedBuf<KsItem> h_ks;
+    PinnedBuf<LinItem> h_lin;
+    uint64_t counters[9] = {0};
+    bool timing = false;
+    Timer timer;
+    int num_sms = 148;
+};
+
+namespace {
+
+int fail(locpir_b200_ctx* c, int code, const std::string& msg)
+{
+    if (c)
+        c->err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(locpir_b200_ctx* c, F&& f)
+{
+    if (!c)
+        return LOCPIR_B200_EINVAL;
+    try {
+        f();
+        return LOCPIR_B200_OK;
+    } catch (const std::invalid_argument& e) {
+        return fail(c, LOCPIR_B200_EINVAL, e.what());
+    } catch (const std::logic_error& e) {
+        return fail(c, LOCPIR_B200_ELOGIC, e.what());
+    } catch (const CudaError& e) {
+        return fail(c, LOCPIR_B200_ECUDA, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(c, LOCPIR_B200_ENOMEM, "out of host memory");
+    } catch (const std::exception& e) {
+        return fail(c, LOCPIR_B200_ECUDA, e.what());
+    }
+}
+
+// Twiddle tables: same formulas as the oracle contract (oracle/tfhe_oracle.c
+// or_fft_tables): W[k] = e^{2 pi i k / 512} with W[k + 128] = i W[k] exactly,
+// TW[j] = e^{i pi j / 1024}, UT[j] = conj(TW[j]) / 512.
+void make_tables(uint32_t N, std::vector<double2>& W, std::vector<double2>& TW,
+                 std::vector<double2>& UT)
+{
+    const uint32_t M = N / 2, Q = M / 4;
+    const double pi = 3.14159265358979323846;
+    W.assign(M / 2, make_double2(0, 0));
+    TW.assign(M, make_double2(0, 0));
+    UT.assign(M, make_double2(0, 0));
+    for (uint32_t k = 0; k < Q; k++) {
+        const double re = k == 0 ? 1.0 : std::cos(2.0 * pi * (double)k / (double)M);
+        const double im = k == 0 ? 0.0 : std::sin(2.0 * pi * (double)k / (double)M);
+        W[k] = make_double2(re, im);
+        W[k + Q] = make_double2(-im, re);
+    }
+    for (uint32_t j = 0; j < M; j++) {
+        const double re = j == 0 ? 1.0 : std::cos(pi * (double)j / (double)N);
+        const double im = j == 0 ? 0.0 : std::sin(pi * (double)j / (double)N);
+        TW[j] = make_double2(re, im);
+        UT[j] = make_double2(re / (double)M, -im / (double)M);
+    }
+}
+
+void need_keys(locpir_b200_ctx* c)
+{
+    if (!c->have_keys)
+        throw std::logic_error("bootstrapping and key-switching keys are not uploaded");
+}
+
+void check_pool(locpir_b200_ctx* c, uint64_t first, uint64_t count)
+{
+    if (first + count > c->pool_slots || first + count < first)
+        throw std::invalid_argument("pool slot range out of bounds");
+}
+
+void timed_begin(locpir_b200_ctx* c, int k)
+{
+    if (!c->timing)
+        return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, c->stream));
+    c->timer.ev[k].push_back(e);
+}
+void timed_end(locpir_b200_ctx* c, int k)
+{
+    if (!c->timing)
+        return;
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(e, c->stream));
+    c->timer.ev[k].push_back(e);
+    c->timer.launches[k]++;
+}
+
+void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
+{
+    if (!count)
+        return;
+    timed_begin(c, 0);
+    const uint32_t mu = 0x20000000u;
+    if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+        k_blind_rotate<3, 7><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
+                                                          c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
+    else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+        k_blind_rotate<2, 10><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
+                                                           c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
+    else
+        throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    CK(cudaGetLastError());
+    timed_end(c, 0);
+}
+
+void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
+{
+    if (!count)
+        return;
+    timed_begin(c, 1);
+    const uint32_t blocks = (count + KS_CT - 1) / KS_CT;
+    const size_t smem = (size_t)KS_CT * c->p.N * sizeof(uint16_t);
+    k_keyswitch<<<blocks, KS_THREADS, smem, c->stream>>>(c->dp, items, count, c->pool_N.p,
+                                                         c->pool_n.p, c->ksk.p);
+    CK(cudaGetLastError());
+    timed_end(c, 1);
+}
+
+void launch_lin(locpir_b200_ctx* c, const LinItem* items, uint32_t count)
+{
+    if (!count)
+        return;
+    timed_begin(c, 2);
+    const uint64_t total = (uint64_t)count * (c->p.n + 1);
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    k_linear<<<blocks, 256, 0, c->stream>>>(c->dp, items, count, c->pool_n.p);
+    CK(cudaGetLastError());
+    timed_end(c, 2);
+}
+
+void validate_slots(locpir_b200_ctx* c, const locpir_b200_gate_op* ops, uint64_t count)
+{
+    for (uint64_t g = 0; g < count; g++) {
+        const auto& op = ops[g];
+        for (uint32_t s : {op.in0, op.in1, op.in2})
+            if (s != SLOT_NONE && s >= c->pool_slots &&
+                !(op.kind == LOCPIR_B200_CONST && s == op.in0))
+                throw std::invalid_argument("operand slot " + std::to_string(s) +
+                                            " outside the pool");
+        if (op.out >= c->pool_slots)
+            throw std::invalid_argument("output slot outside the pool");
+    }
+}
+
+}  // namespace
+
+// A planned program: per-wave item ranges in device memory.
+struct locpir_b200_program {
+    Plan plan;
+    int device = 0;
+    DevBuf<BrItem> br;
+    DevBuf<KsItem> ks;
+    DevBuf<LinItem> lin;
+    std::vector<size_t> ob, ok, ol;  // per-wave offsets
+    uint64_t kernels = 0;
+};
+
+namespace {
+
+void program_upload(locpir_b200_ctx* c, locpir_b200_program* pr, BrItem* hb, KsItem* hk,
+                    LinItem* hl, DevBuf<BrItem>& db, DevBuf<KsItem>& dk, DevBuf<LinItem>& dl)
+{
+    const Plan& P = pr->plan;
+    size_t ob = 0, ok = 0, ol = 0;
+    pr->ob.clear();
+    pr->ok.clear();
+    pr->ol.clear();
+    pr->kernels = 0;
+    for (uint32_t w = 0; w < P.waves(); w++) {
+        pr->ob.push_back(ob);
+        pr->ok.push_back(ok);
+        pr->ol.push_back(ol);
+        std::copy(P.br[w].begin(), P.br[w].end(), hb + ob);
+        std::copy(P.ks[w].begin(), P.ks[w].end(), hk + ok);
+        std::copy(P.lin[w].begin(), P.lin[w].end(), hl + ol);
+        ob += P.br[w].size();
+        ok += P.ks[w].size();
+        ol += P.lin[w].size();
+        pr->kernels += !P.br[w].empty() + !P.ks[w].empty() + !P.lin[w].empty();
+    }
+    db.reserve(ob + 1, c->stream, false);
+    dk.reserve(ok + 1, c->stream, false);
+    dl.reserve(ol + 1, c->stream, false);
+    if (ob)
+        CK(cudaMemcpyAsync(db.p, hb, ob * sizeof(BrItem), cudaMemcpyHostToDevice, c->stream));
+    if (ok)
+        CK(cudaMemcpyAsync(dk.p, hk, ok * sizeof(KsItem), cudaMemcpyHostToDevice, c->stream));
+    if (ol)
+        CK(cudaMemcpyAsync(dl.p, hl, ol * sizeof(LinItem), cudaMemcpyHostToDevice, c->stream));
+}
+
+void program_enqueue(locpir_b200_ctx* c, const locpir_b200_program* pr, const BrItem* db,
+                     const KsItem* dk, const LinItem* dl)
+{
+    const Plan& P = pr->plan;
+    if (P.n_br)
+        need_keys(c);
+    if (P.scratch > c->scratch_slots) {
+        c->pool_N.reserve((size_t)P.scratch * c->dp.N_stride, c->stream, false);
+        c->scratch_slots = c->pool_N.n / c->dp.N_stride;
+    }
+    for (uint32_t w = 0; w < P.waves(); w++) {
+        launch_lin(c, dl + pr->ol[w], (uint32_t)P.lin[w].size());
+        launch_br(c, db + pr->ob[w], (uint32_t)P.br[w].size());
+        launch_ks(c, dk + pr->ok[w], (uint32_t)P.ks[w].size());
+    }
+    for (int i = 0; i < 9; i++)
+        c->counters[i] += P.counts[i];
+}
+
+size_t plan_items(const Plan& P, size_t& nb, size_t& nk, size_t& nl)
+{
+    nb = nk = nl = 0;
+    for (uint32_t w = 0; w < P.waves(); w++) {
+        nb += P.br[w].size();
+        nk += P.ks[w].size();
+        nl += P.lin[w].size();
+    }
+    return nb + nk + nl;
+}
+
+void execute(locpir_b200_ctx* c, const locpir_b200_gate_op* ops, uint64_t count)
+{
+    validate_slots(c, ops, count);
+    locpir_b200_program pr;
+    pr.plan = build_plan(ops, count);  // throws invalid_argument on malformed programs
+    size_t nb, nk, nl;
+    plan_items(pr.plan, nb, nk, nl);
+    CK(cudaStreamSynchronize(c->stream));  // pinned staging may still feed an earlier copy
+    c->h_br.reserve(nb + 1);
+    c->h_ks.reserve(nk + 1);
+    c->h_lin.reserve(nl + 1);
+    program_upload(c, &pr, c->h_br.p, c->h_ks.p, c->h_lin.p, c->d_br, c->d_ks, c->d_lin);
+    program_enqueue(c, &pr, c->d_br.p, c->d_ks.p, c->d_lin.p);
+}
+
+void pool_copy(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_t* src,
+               uint32_t* dst, cudaMemcpyKind kind, bool to_pool)
+{
+    check_pool(c, first, count);
+    if (!count)
+        return;
+    const size_t wb = (size_t)(c->p.n + 1) * 4, pb = (size_t)c->dp.n_stride * 4;
+    if (to_pool)
+        CK(cudaMemcpy2DAsync(c->pool_n.p + first * c->dp.n_stride, pb, src, wb, wb, count, kind,
+                             c->stream));
+    else
+        CK(cudaMemcpy2DAsync(dst, wb, c->pool_n.p + first * c->dp.n_stride, pb, wb, count, kind,
+                             c->stream));
+}
+
+}  // namespace
+
+extern "C" {
+
+int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream,
+                           locpir_b200_ctx** out)
+{
+    if (!p || !out || !locpir_b200_bk_words(p))
+        return LOCPIR_B200_EINVAL;
+    *out = nullptr;
+    auto c = std::make_unique<locpir_b200_ctx>();
+    c->p = *p;
+    c->device = device;
+    const uint32_t ns = (p->n + 1 + 3) & ~3u;
+    c->dp = {p->n, p->N, p->bk_l, p->bk_bgbit, p->ks_t, p->ks_basebit, ns, p->N + 4};
+    int rc = guarded(c.get(), [&] {
+        CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        if (stream) {
+            c->stream = (cudaStream_t)stream;
+        } else {
+            CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        std::vector<double2> W, TW, UT;
+        make_tables(p->N, W, TW, UT);
+        c->W.reserve(W.size(), c->stream, false);
+        c->TW.reserve(TW.size(), c->stream, false);
+        c->UT.reserve(UT.size(), c->stream, false);
+        CK(cudaMemcpy(c->W.p, W.data(), W.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->TW.p, TW.data(), TW.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->UT.p, UT.data(), UT.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(KS_CT * p->N * sizeof(uint16_t))));
+    });
+    if (rc != LOCPIR_B200_OK) {
+        fprintf(stderr, "locpir_b200_ctx_create: %s\n", c->err.c_str());
+        if (c->own_stream && c->stream)
+            cudaStreamDestroy(c->stream);
+        return rc;
+    }
+    *out = c.release();
+    return LOCPIR_B200_OK;
+}
+
+void locpir_b200_ctx_destroy(locpir_b200_ctx* c)
+{
+    if (!c)
+        return;
+    cudaSetDevice(c->device);
+    if (c->stream)
+        cudaStreamSynchronize(c->stream);
+    for (auto& v : c->timer.ev)
+        for (auto e : v)
+            cudaEventDestroy(e);
+    if (c->own_stream && c->stream)
+        cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* locpir_b200_last_error(const locpir_b200_ctx* c) { return c ? c->err.c_str() : ""; }
+
+void* locpir_b200_stream(const locpir_b200_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32_t* ksk,
+                            int on_device)
+{
+    return guarded(c, [&] {
+        if (!bk || !ksk)
+            throw std::invalid_argument("null key pointer");
+        CK(cudaSetDevice(c->device));
+        const size_t bkw = locpir_b200_bk_words(&c->p);
+        const uint32_t rows = 2 * c->p.bk_l;
+        const size_t polys = (size_t)c->p.n * rows * 2;
+        DevBuf<uint32_t> tmp;
+        const uint32_t* dbk = bk;
+        if (!on_device) {
+            tmp.reserve(bkw, c->stream, false);
+            CK(cudaMemcpyAsync(tmp.p, bk, bkw * 4, cudaMemcpyHostToDevice, c->stream));
+            dbk = tmp.p;
+        }
+        c->bkf.reserve(polys * FFT_M, c->stream, false);
+        k_bk_to_freq<<<(uint32_t)polys, 64, 0, c->stream>>>(dbk, c->bkf.p, c->W.p, c->TW.p);
+        CK(cudaGetLastError());
+        // KSK rows padded to n_stride words (zero padding)
+        const size_t rows_ks = (size_t)c->p.N * c->p.ks_t * ((1u << c->p.ks_basebit) - 1);
+        c->ksk.reserve(rows_ks * c->dp.n_stride, c->stream, false);
+        CK(cudaMemsetAsync(c->ksk.p, 0, rows_ks * c->dp.n_stride * 4, c->stream));
+        CK(cudaMemcpy2DAsync(c->ksk.p, (size_t)c->dp.n_stride * 4, ksk, (size_t)(c->p.n + 1) * 4,
+                             (size_t)(c->p.n + 1) * 4, rows_ks,
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                             c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->have_keys = true;
+    });
+}
+
+int locpir_b200_pool_reserve(locpir_b200_ctx* c, uint64_t slots)
+{
+    return guarded(c, [&] {
+        CK(cudaSetDevice(c->device));
+        if (slots <= c->pool_slots)
+            return;
+        c->pool_n.reserve((size_t)slots * c->dp.n_stride, c->stream, true);
+        const uint64_t old = c->pool_slots;
+        c->pool_slots = c->pool_n.n / c->dp.n_stride;
+        CK(cudaMemsetAsync(c->pool_n.p + old * c->dp.n_stride, 0,
+                           (c->pool_slots - old) * c->dp.n_stride * 4, c->stream));
+    });
+}
+
+uint64_t locpir_b200_pool_capacity(const locpir_b200_ctx* c) { return c ? c->pool_slots : 0; }
+
+int locpir_b200_pool_h2d(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_t* host)
+{
+    return guarded(c, [&] {
+        pool_copy(c, first, count, host, nullptr, cudaMemcpyHostToDevice, true);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int locpir_b200_pool_d2h(locpir_b200_ctx* c, uint64_t first, uint64_t count, uint32_t* host)
+{
+    return guarded(c, [&] {
+        pool_copy(c, first, count, nullptr, host, cudaMemcpyDeviceToHost, false);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int locpir_b200_pool_load_device(locpir_b200_ctx* c, uint64_t first, uint64_t count,
+                                 const uint32_t* dev)
+{
+    return guarded(c, [&] { pool_copy(c, first, count, dev, nullptr, cudaMemcpyDeviceToDevice, true); });
+}
+
+int locpir_b200_pool_store_device(locpir_b200_ctx* c, uint64_t first, uint64_t count,
+                                  uint32_t* dev)
+{
+    return guarded(c, [&] { pool_copy(c, first, count, nullptr, dev, cudaMemcpyDeviceToDevice, false); });
+}
+
+int locpir_b200_run(locpir_b200_ctx* c, const locpir_b200_gate_op* ops, uint64_t count)
+{
+    return guarded(c, [&] {
+        if (count && !ops)
+            throw std::invalid_argument("null program");
+        CK(cudaSetDevice(c->device));
+        execute(c, ops, count);
+    });
+}
+
+int locpir_b200_eval_level(locpir_b200_ctx* c, const locpir_b200_gate_op* ops, uint64_t count)
+{
+    return guarded(c, [&] {
+        if (count && !ops)
+            throw std::invalid_argument("null program");
+        Plan P = build_plan(ops, count);
+        if (P.waves() > 1)
+            throw std::invalid_argument("eval_level: gates of one level must be independent");
+        CK(cudaSetDevice(c->device));
+        execute(c, ops, count);
+    });
+}
+
+int locpir_b200_sync(locpir_b200_ctx* c)
+{
+    return guarded(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int locpir_b200_program_create(locpir_b200_ctx* c, const locpir_b200_gate_op* ops,
+                               uint64_t count, locpir_b200_program** out)
+{
+    return guarded(c, [&] {
+        if (!out || (count && !ops))
+            throw std::invalid_argument("bad program arguments");
+        CK(cudaSetDevice(c->device));
+        validate_slots(c, ops, count);
+        auto pr = std::make_unique<locpir_b200_program>();
+        pr->plan = build_plan(ops, count);
+        pr->device = c->device;
+        size_t nb, nk, nl;
+        plan_items(pr->plan, nb, nk, nl);
+        std::vector<BrItem> hb(nb + 1);
+        std::vector<KsItem> hk(nk + 1);
+        std::vector<LinItem> hl(nl + 1);
+        program_upload(c, pr.get(), hb.data(), hk.data(), hl.data(), pr->br, pr->ks, pr->lin);
+        CK(cudaStreamSynchronize(c->stream));
+        // drop the host-side lists; keep sizes for launching
+        *out = pr.release();
+    });
+}
+
+int locpir_b200_program_launch(locpir_b200_ctx* c, locpir_b200_program* pr)
+{
+    return guarded(c, [&] {
+        if (!pr)
+            throw std::invalid_argument("null program");
+        program_enqueue(c, pr, pr->br.p, pr->ks.p, pr->lin.p);
+    });
+}
+
+uint64_t locpir_b200_program_kernels(const locpir_b200_program* pr) { return pr ? pr->kernels : 0; }
+
+void locpir_b200_program_destroy(locpir_b200_program* pr)
+{
+    if (!pr)
+        return;
+    cudaSetDevice(pr->device);
+    cudaDeviceSynchronize();
+    delete pr;
+}
+
+int locpir_b200_plan(const locpir_b200_gate_op* ops, uint64_t count, uint32_t* levels,
+                     uint64_t* blind_rotations, uint64_t* key_switches)
+{
+    try {
+        Plan P = build_plan(ops, count);
+        if (levels)
+            *levels = P.waves();
+        if (blind_rotations)
+            *blind_rotations = P.n_br;
+        if (key_switches)
+            *key_switches = P.n_ks;
+        return LOCPIR_B200_OK;
+    } catch (const std::invalid_argument&) {
+        return LOCPIR_B200_EINVAL;
+    } catch (...) {
+        return LOCPIR_B200_ELOGIC;
+    }
+}
+
+int locpir_b200_counters(const locpir_b200_ctx* c, uint64_t out[9])
+{
+    if (!c || !out)
+        return LOCPIR_B200_EINVAL;
+    for (int i = 0; i < 9; i++)
+        out[i] = c->counters[i];
+    return LOCPIR_B200_OK;
+}
+
+int locpir_b200_counters_reset(locpir_b200_ctx* c)
+{
+    if (!c)
+        return LOCPIR_B200_EINVAL;
+    for (auto& x : c->counters)
+        x = 0;
+    return LOCPIR_B200_OK;
+}
+
+int locpir_b200_gate_batch_host(locpir_b200_ctx* c, uint32_t kind, const uint32_t* a,
+                                const uint32_t* b, uint32_t* out, uint64_t count)
+{
+    return guarded(c, [&] {
+        GateForm f;
+        if (!gate_form(kind, f))
+            throw std::invalid_argument("gate_batch_host takes a two-input bootstrapped gate");
+        if (count >= (1ull << 30) || (count && (!a || !b || !out)))
+            throw std::invalid_argument("bad batch");
+        CK(cudaSetDevice(c->device));
+        if (c->pool_slots < 3 * count) {
+            int rc = locpir_b200_pool_reserve(c, 3 * count);
+            if (rc)
+                throw CudaError(c->err);
+        }
+        pool_copy(c, 0, count, a, nullptr, cudaMemcpyHostToDevice, true);
+        pool_copy(c, count, count, b, nullptr, cudaMemcpyHostToDevice, true);
+        std::vector<locpir_b200_gate_op> ops(count);
+        for (uint64_t g = 0; g < count; g++)
+            ops[g] = {kind, (uint32_t)g, (uint32_t)(count + g), SLOT_NONE, (uint32_t)(2 * count + g)};
+        execute(c, ops.data(), count);
+        pool_copy(c, 2 * count, count, nullptr, out, cudaMemcpyDeviceToHost, false);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+uint64_t locpir_b200_loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
+{
+    return loc_pir_scratch(Q, R, l, m);
+}
+
+int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                const uint32_t* x_slots, const uint32_t* y_slots,
+                                const uint32_t* bnd_slots, const uint32_t* svc_slots,
+                                const uint32_t* out_slots, uint64_t scratch_first, int xor_tree,
+                                locpir_b200_gate_op* ops, uint64_t* count)
+{
+    if (!count || !Q || !R || l < 2 || !m || !x_slots || !y_slots || !bnd_slots || !svc_slots ||
+        !out_slots)
+        return LOCPIR_B200_EINVAL;
+    try {
+        std::vector<locpir_b200_gate_op> v;
+        emit_loc_pir(v, Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
+                     scratch_first, xor_tree);
+        if (ops) {
+            if (*count < v.size())
+                return LOCPIR_B200_EINVAL;
+            std::copy(v.begin(), v.end(), ops);
+        }
+        *count = v.size();
+        return LOCPIR_B200_OK;
+    } catch (...) {
+        return LOCPIR_B200_EINVAL;
+    }
+}
+
+int locpir_b200_loc_pir(locpir_b200_ctx* c, uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                        const uint32_t* x_slots, const uint32_t* y_slots,
+                        const uint32_t* bnd_slots, const uint32_t* svc_slots,
+                        uint32_t* out_slots, uint64_t scratch_first, int xor_tree)
+{
+    return guarded(c, [&] {
+        if (!Q || !R || l < 2 || !m || !x_slots || !y_slots || !bnd_slots || !svc_slots ||
+            !out_slots)
+            throw std::invalid_argument("loc_pir: bad arguments");
+        if (scratch_first + loc_pir_scratch(Q, R, l, m) > c->pool_slots)
+            throw std::invalid_argument("loc_pir: pool too small for the circuit's scratch");
+        std::vector<locpir_b200_gate_op> v;
+        emit_loc_pir(v, Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
+                     scratch_first, xor_tree);
+        CK(cudaSetDevice(c->device));
+        execute(c, v.data(), v.size());
+    });
+}
+
+int locpir_b200_timing_enable(locpir_b200_ctx* c, int on)
+{
+    if (!c)
+        return LOCPIR_B200_EINVAL;
+    c->timing = on != 0;
+    return LOCPIR_B200_OK;
+}
+
+int locpir_b200_kernel_stats(locpir_b200_ctx* c, double ms[3], uint64_t launches[3])
+{
+    return guarded(c, [&] {
+        CK(cudaSetDevice(c->device));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int k = 0; k < 3; k++) {
+            auto& v = c->timer.ev[k];
+            for (size_t i = 0; i + 1 < v.size(); i += 2) {
+                float t = 0;
+                CK(cudaEventElapsedTime(&t, v[i], v[i + 1]));
+                c->timer.ms[k] += t;
+            }
+            for (auto e : v)
+                cudaEventDestroy(e);
+            v.clear();
+            if (ms)
+                ms[k] = c->timer.ms[k];
+            if (launches)
+                launches[k] = c->timer.launches[k];
+            c->timer.ms[k] = 0;
+            c->timer.launches[k] = 0;
+        }
+    });
+}
+
+int locpir_b200_fp64_peak(locpir_b200_ctx* c, double* tflops)
+{
+    return guarded(c, [&] {
+        if (!tflops)
+            throw std::invalid_argument("null output");
+        CK(cudaSetDevice(c->device));
+        DevBuf<double> sink;
+        sink.reserve(1, c->stream, false);
+        const int iters = 1 << 16, threads = 256, blocks = c->num_sms * 8;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        k_fp64_peak<<<blocks, threads, 0, c->stream>>>(sink.p, 256);  // warm-up
+        double best = 0;
+        for (int rep = 0; rep < 3; rep++) {
+            CK(cudaEventRecord(e0, c->stream));
+            k_fp64_peak<<<blocks, threads, 0, c->stream>>>(sink.p, iters);
+            CK(cudaEventRecord(e1, c->stream));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            const double flops = 2.0 * 8.0 * iters * (double)threads * blocks;
+            best = std::max(best, flops / (ms * 1e-3) / 1e12);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *tflops = best;
+    });
+}
+
+}  // extern "C"

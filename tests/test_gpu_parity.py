@@ -1,0 +1,267 @@
+"""Parity of the B200 path against the CPU oracle and the reference's own pins.
+
+Every test calls through the C ABI (include/locpir_b200.h) via the package's
+ctypes binding.  Bars:
+  * ciphertexts bit-exact with the oracle (FFT and exact modes agree, see
+    test_oracle_tfhe.py), hence pre-KS coefficients within 0 of the exact product;
+  * decrypted bits equal to the plaintext function (the reference clear engine)
+    for truth tables, comparators and loc_pir (test_gate_engine.cpp,
+    test_circuits.cpp, acceptance.cpp);
+  * gate counters equal to the reference accounting (gate_engine.hpp:31-77).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GATE_FN = {
+    "and": lambda a, b: a & b, "or": lambda a, b: a | b, "xor": lambda a, b: a ^ b,
+    "xnor": lambda a, b: 1 - (a ^ b), "nand": lambda a, b: 1 - (a & b),
+    "nor": lambda a, b: 1 - (a | b),
+}
+
+
+def _signed(x):
+    return ((np.asarray(x, np.int64) + 2 ** 31) % 2 ** 32) - 2 ** 31
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2407_19871_b200 import ClientKeys, Context, TfheParams
+    out = {}
+    for lvl in (80, 128):
+        p = TfheParams(lvl)
+        keys = ClientKeys(p, 7)
+        ctx = Context(p, 0)
+        ctx.upload_keys(keys.bk, keys.ksk)
+        out[lvl] = (p, keys, ctx)
+    yield out
+    for _, _, ctx in out.values():
+        ctx.close()
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_gates_bit_exact_with_oracle(dev, level, okeys80, okeys128):
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[level]
+    ok = okeys80 if level == 80 else okeys128
+    bits = np.array([0, 0, 1, 1, 0, 1], np.uint8)
+    bits2 = np.array([0, 1, 0, 1, 1, 1], np.uint8)
+    a = keys.encrypt_bits(bits, 100 + level)
+    b = keys.encrypt_bits(bits2, 200 + level)
+    for name, kind in [("and", _abi.AND), ("nand", _abi.NAND), ("xnor", _abi.XNOR)]:
+        out = ctx.gate_batch_host(kind, a, b)
+        assert list(keys.decrypt_bits(out)) == [GATE_FN[name](x, y) for x, y in zip(bits, bits2)]
+        for g in (0, 3):
+            assert np.array_equal(out[g], ok.gate(name, a[g], b[g])), (name, g)
+
+
+def test_mux_bit_exact_with_oracle(dev, okeys128):
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[128]
+    s, x, y = (keys.encrypt_bits([v], 300 + i) for i, v in enumerate([1, 0, 1]))
+    ctx.pool_reserve(8)
+    ctx.h2d(0, np.concatenate([s, x, y]))
+    ctx.run([(_abi.MUX, 0, 1, 2, 3), (_abi.MUX, 1, 0, 2, 4)])
+    out = ctx.d2h(3, 2)
+    assert np.array_equal(out[0], okeys128.gate("mux", s[0], x[0], y[0]))
+    assert np.array_equal(out[1], okeys128.gate("mux", x[0], s[0], y[0]))
+    assert list(keys.decrypt_bits(out)) == [0, 1]
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_truth_tables_many_seeds(dev, level):
+    """acceptance.cpp:334-375: every gate, both inputs, many encryption seeds."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[level]
+    seeds = 100
+    A = np.tile([0, 0, 1, 1], seeds).astype(np.uint8)
+    B = np.tile([0, 1, 0, 1], seeds).astype(np.uint8)
+    S = np.repeat([0, 1], 2 * seeds).astype(np.uint8)
+    a = keys.encrypt_bits(A, 1 + level)
+    b = keys.encrypt_bits(B, 2 + level)
+    s = keys.encrypt_bits(S, 3 + level)
+    M = len(A)
+    ctx.pool_reserve(20 * M)
+    ctx.h2d(0, a)
+    ctx.h2d(M, b)
+    ctx.h2d(2 * M, s)
+    kinds = [("and", _abi.AND), ("or", _abi.OR), ("xor", _abi.XOR), ("xnor", _abi.XNOR),
+             ("nand", _abi.NAND), ("nor", _abi.NOR)]
+    ops = []
+    for k, (_, kind) in enumerate(kinds):
+        ops += [(kind, g, M + g, 0, (3 + k) * M + g) for g in range(M)]
+    ops += [(_abi.MUX, 2 * M + g, g, M + g, 9 * M + g) for g in range(M)]
+    ops += [(_abi.NOT, g, 0, 0, 10 * M + g) for g in range(M)]
+    ctx.counters_reset()
+    ctx.run(ops)
+    for k, (name, _) in enumerate(kinds):
+        got = keys.decrypt_bits(ctx.d2h((3 + k) * M, M))
+        assert np.array_equal(got, [GATE_FN[name](x, y) for x, y in zip(A, B)]), name
+    mux = keys.decrypt_bits(ctx.d2h(9 * M, M))
+    assert np.array_equal(mux, np.where(S == 1, A, B))
+    nots = keys.decrypt_bits(ctx.d2h(10 * M, M))
+    assert np.array_equal(nots, 1 - A)
+    c = ctx.counters()
+    assert c["and"] == M and c["mux"] == M and c["not"] == M
+    assert c["bootstrap_units"] == 6 * M + 2 * M
+    # output noise stays far inside the 1/16 decision margin (acceptance.cpp:377-410)
+    outs = ctx.d2h(3 * M, 6 * M)
+    ph = np.array([_signed(keys.phase(o)) for o in outs]) / 2 ** 32
+    assert np.abs(np.abs(ph) - 0.125).max() < 1 / 16
+
+
+def test_long_xor_chain_stays_decryptable(dev):
+    """test_gate_engine.cpp:87-97: 1000 dependent XORs (eager, one gate per program)."""
+    from paper_2407_19871_b200 import GateEngine
+    p, keys, ctx = dev[128]
+    eng = GateEngine(ctx, keys, seed=5)
+    eng._next_slot = 0
+    acc = eng.encrypt(False)
+    one = eng.encrypt(True)
+    for _ in range(1000):
+        acc = eng.hom_xor(acc, one)
+    assert eng.decrypt(acc) is False
+    acc = eng.hom_xor(acc, one)
+    assert eng.decrypt(acc) is True
+
+
+def _words(patterns, l):
+    return np.array([[(pt >> i) & 1 for i in range(l)] for pt in patterns], np.uint8)
+
+
+def _signed_of(pattern, l):
+    return pattern - (1 << l) if pattern >> (l - 1) else pattern
+
+
+@pytest.mark.parametrize("l", [2, 3, 4, 5, 6])
+def test_comparator_exhaustive(dev, l):
+    """acceptance.cpp:113-150: every signed l-bit pair, hom_less and hom_less_equal."""
+    from paper_2407_19871_b200 import Context
+    _run_comparator_pairs(dev[80], l, [(pa, pb) for pa in range(1 << l) for pb in range(1 << l)],
+                          seed=40 + l)
+
+
+def test_comparator_random_16bit(dev):
+    """acceptance.cpp:152-160: 1000 random 16-bit pairs."""
+    rng = np.random.default_rng(24)
+    pairs = [(int(rng.integers(0, 1 << 16)), int(rng.integers(0, 1 << 16))) for _ in range(1000)]
+    _run_comparator_pairs(dev[128], 16, pairs, seed=24)
+
+
+def _run_comparator_pairs(d, l, pairs, seed):
+    from paper_2407_19871_b200 import GateEngine
+    from paper_2407_19871_b200.circuits import (CipherWord, FixedPointFormat, hom_less,
+                                                hom_less_equal)
+    p, keys, ctx = d
+    eng = GateEngine(ctx, keys, seed=seed)
+    fmt = FixedPointFormat(l - 1, 1)
+    A = _words([a for a, _ in pairs], l)
+    B = _words([b for _, b in pairs], l)
+    ca = eng.encrypt_many(A.reshape(-1))
+    cb = eng.encrypt_many(B.reshape(-1))
+    lt, le = [], []
+    with eng.batch():
+        for i in range(len(pairs)):
+            wa = CipherWord(ca[i * l:(i + 1) * l], fmt)
+            wb = CipherWord(cb[i * l:(i + 1) * l], fmt)
+            lt.append(hom_less(wa, wb, eng))
+            le.append(hom_less_equal(wa, wb, eng))
+    got_lt = eng.decrypt_many(lt)
+    got_le = eng.decrypt_many(le)
+    for i, (pa, pb) in enumerate(pairs):
+        sa, sb = _signed_of(pa, l), _signed_of(pb, l)
+        assert got_lt[i] == (sa < sb), (pa, pb)
+        assert got_le[i] == (sa <= sb), (pa, pb)
+
+
+def _encode_regions(eng, spec, fmt, m):
+    """spec: list of (x1, x2, y1, y2, service) in grid units -> EncodedRegion (trivial
+    boundary words, dataset.hpp:250-253; trivial services, circuits.hpp:150-163)."""
+    from paper_2407_19871_b200.circuits import (EncodedRegion, PlainWord, constant_word,
+                                                trivial_services)
+    out = []
+    svc = trivial_services([s[4] for s in spec], m, eng)
+    for i, (x1, x2, y1, y2, _) in enumerate(spec):
+        w = [constant_word(PlainWord.from_integer(v, fmt), eng) for v in (x1, x2, y1, y2)]
+        out.append(EncodedRegion(*w, svc[i], i))
+    return out
+
+
+@pytest.mark.parametrize("tree", [False, True])
+def test_loc_pir_reference_regions(dev, tree):
+    """test_circuits.cpp:150-213: retrieval, zero outside, half-open edges, counts."""
+    from paper_2407_19871_b200 import GateEngine
+    from paper_2407_19871_b200.circuits import (FixedPointFormat, PlainWord, decrypt_service,
+                                                encrypt_word, loc_pir)
+    p, keys, ctx = dev[80]
+    fmt = FixedPointFormat(4, 2)
+    spec = [(0, 8, 0, 8, 5), (8, 16, 0, 8, 3), (-16, -4, -12, -4, 7)]
+    cases = [((5, 2), 5), ((9, 1), 3), ((-10, -6), 7), ((28, 28), 0), ((0, 0), 5), ((8, 0), 3),
+             ((16, 0), 0), ((5, 8), 0)]
+    eng = GateEngine(ctx, keys, seed=29)
+    regions = _encode_regions(eng, spec, fmt, 3)
+    ctx.counters_reset()
+    outs = []
+    with eng.batch():
+        for (gx, gy), _ in cases:
+            x = encrypt_word(PlainWord.from_integer(gx, fmt), eng)
+            y = encrypt_word(PlainWord.from_integer(gy, fmt), eng)
+            outs.append(loc_pir(x, y, regions, eng, tree=tree))
+    for out, (_, want) in zip(outs, cases):
+        assert decrypt_service(out, eng) == want
+    c = eng.counters()
+    N, l, m = 3, 6, 3
+    assert c["xnor"] == len(cases) * N * 4 * l and c["mux"] == len(cases) * N * 4 * l
+    assert c["and"] == len(cases) * N * (3 + m) and c["xor"] == len(cases) * N * m
+    assert c["bootstrap_units"] == len(cases) * N * (12 * l + 2 * m + 3)
+
+
+def test_loc_pir_synthetic_matches_reference_golden(dev, golden):
+    """bench.hpp:345-384 synthetic cases; retrieved value must equal the reference's."""
+    from paper_2407_19871_b200 import GateEngine
+    from paper_2407_19871_b200.circuits import (PlainWord, decrypt_service, encrypt_word,
+                                                format_for_length, loc_pir)
+    p, keys, ctx = dev[80]
+    rows = np.array(golden["locpir_synthetic_N_l_m_got_expected_units_xnor_mux_and_xor_not_pred"])
+    for N, l, m, got_ref, exp, units, *_ in rows.reshape(-1, 12)[:12]:
+        N, l, m = int(N), int(l), int(m)
+        fmt = format_for_length(l)
+        eng = GateEngine(ctx, keys, seed=1000 + N * 100 + l)
+        spec = [(4 * i, 4 * i + 4, 4 * i, 4 * i + 4, (37 * i + 11) & ((1 << m) - 1))
+                for i in range(N)]
+        regions = _encode_regions(eng, spec, fmt, m)
+        pt = PlainWord.from_integer(((N - 1) // 2) * 4 + 2, fmt)
+        ctx.counters_reset()
+        out = loc_pir(encrypt_word(pt, eng), encrypt_word(pt, eng), regions, eng, tree=True)
+        assert decrypt_service(out, eng) == got_ref == exp
+        assert eng.counters()["bootstrap_units"] == units
+
+
+def test_cfg2_full_size_nand_batch(dev, okeys128):
+    """BASELINE configs[1]: 65,536 NAND at 128-bit -- every output decrypts right and a
+    sample is bit-exact with the oracle."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[128]
+    G = 65536
+    rng = np.random.default_rng(2)
+    A = rng.integers(0, 2, G).astype(np.uint8)
+    B = rng.integers(0, 2, G).astype(np.uint8)
+    a = keys.encrypt_bits(A, 77)
+    b = keys.encrypt_bits(B, 78)
+    out = ctx.gate_batch_host(_abi.NAND, a, b)
+    assert np.array_equal(keys.decrypt_bits(out), 1 - (A & B))
+    for g in (0, G // 2 + 1, G - 1):
+        assert np.array_equal(out[g], okeys128.gate("nand", a[g], b[g]))
+
+
+def test_errors_map_to_reference_exceptions(dev):
+    from paper_2407_19871_b200 import GateEngine, InvalidArgument, _abi
+    p, keys, ctx = dev[128]
+    e1 = GateEngine(ctx, keys, seed=1)
+    e2 = GateEngine(ctx, keys, seed=2)
+    a = e1.encrypt(True)
+    with pytest.raises(InvalidArgument):
+        e2.hom_and(a, a)  # cipher bit belongs to a different engine
+    with pytest.raises(InvalidArgument):
+        ctx.run([(_abi.AND, 0, 1, 0, ctx.pool_capacity + 5)])

@@ -1,0 +1,94 @@
+"""The oracle's restatement of TFHE gate bootstrapping (SURVEY.md §8(a')).
+
+Parity of these internals against TFHE 1.1 is unpinned (the library is absent
+from /root/reference); they are anchored on the reference's gate-level
+behaviour (truth tables, gate_engine.hpp:196-269) and on internal consistency:
+the FP64-FFT external product must equal the exact mod-2^32 product."""
+import numpy as np
+import pytest
+
+
+def _signed(x):
+    return ((np.asarray(x, np.int64) + 2 ** 31) % 2 ** 32) - 2 ** 31
+
+
+def test_fft_roundtrip_and_tables(oracle):
+    W, TW, UT = oracle.fft_tables(1024)
+    assert W.shape == (256, 2) and tuple(W[0]) == (1.0, 0.0) and tuple(W[128]) == (-0.0, 1.0)
+    for k in range(128):  # W[k + 128] = i * W[k] exactly
+        assert W[k + 128][0] == -W[k][1] and W[k + 128][1] == W[k][0]
+    rng = np.random.default_rng(1)
+    a = rng.integers(-2 ** 31, 2 ** 31, 1024).astype(np.int32)
+    F = oracle.fft_forward(a)
+    acc = np.zeros(1024, np.uint32)
+    oracle.fft_inverse_add(F, acc)
+    assert np.array_equal(acc.view(np.int32), a)
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_fft_product_equals_exact_product(oracle, level, okeys80, okeys128):
+    K = okeys80 if level == 80 else okeys128
+    rng = np.random.default_rng(level)
+    for i in (0, 1, K.n - 1):
+        tr = rng.integers(0, 2 ** 32, 2 * K.N, dtype=np.uint64).astype(np.uint32)
+        e = K.external_product(i, tr, oracle.EXACT)
+        f = K.external_product(i, tr, oracle.FFT)
+        assert np.array_equal(e, f)
+
+
+def test_full_blind_rotation_fft_equals_exact(oracle, okeys80):
+    K = okeys80
+    s = oracle.NoiseSampler(5, K.p.alpha_in)
+    ct = K.encrypt(1, s)
+    assert np.array_equal(K.blind_rotate_acc(ct, mode=oracle.EXACT),
+                          K.blind_rotate_acc(ct, mode=oracle.FFT))
+
+
+def test_decomposition_reconstructs(oracle, okeys128):
+    K = okeys128
+    p = K.p
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 2 ** 32, K.N, dtype=np.uint64).astype(np.uint32)
+    rec = np.zeros(K.N, np.int64)
+    for lev in range(p.l):
+        d = K.decompose(x, lev)
+        assert d.min() >= -(1 << (p.bgbit - 1)) and d.max() < (1 << (p.bgbit - 1))
+        rec += d.astype(np.int64) << (32 - (lev + 1) * p.bgbit)
+    err = _signed(rec - x.astype(np.int64))
+    assert np.abs(err).max() <= 1 << (31 - p.l * p.bgbit)
+
+
+def test_mod_switch(oracle):
+    assert oracle.mod_switch(0, 1024) == 0
+    assert oracle.mod_switch(0x20000000, 1024) == 256
+    assert oracle.mod_switch(0xFFFFFFFF, 1024) == 0  # wraps to 2N == 0
+    assert oracle.mod_switch((1 << 20) - 1, 1024) == 0
+    assert oracle.mod_switch(1 << 20, 1024) == 1
+
+
+def test_keyswitch_preserves_phase(oracle, okeys128):
+    K = okeys128
+    # an N-dim encryption of +1/8 under the TRLWE key, then key switch to the LWE key
+    rng = np.random.default_rng(4)
+    a = rng.integers(0, 2 ** 32, K.N, dtype=np.uint64).astype(np.uint32)
+    body = (int(np.sum(a.astype(np.uint64) * K.trlwe_key)) + 0x20000000) % 2 ** 32
+    out = K.keyswitch(np.append(a, np.uint32(body)))
+    ph = _signed(K.phase(out)) / 2 ** 32
+    assert abs(ph - 0.125) < 1 / 64
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_bootstrapped_gate_truth_tables(oracle, level, okeys80, okeys128):
+    K = okeys80 if level == 80 else okeys128
+    s = oracle.NoiseSampler(21, K.p.alpha_in)
+    for kind, fn in [("and", lambda a, b: a & b), ("xor", lambda a, b: a ^ b),
+                     ("nand", lambda a, b: 1 - (a & b)), ("xnor", lambda a, b: 1 - (a ^ b))]:
+        for a in (0, 1):
+            for b in (0, 1):
+                out = K.gate(kind, K.encrypt(a, s), K.encrypt(b, s))
+                assert K.decrypt(out) == fn(a, b), (kind, a, b)
+                ph = _signed(K.phase(out)) / 2 ** 32
+                assert abs(abs(ph) - 0.125) < 1 / 16  # acceptance.cpp:377-410 noise bound
+    sel = K.encrypt(1, s)
+    assert K.decrypt(K.gate("mux", sel, K.encrypt(0, s), K.encrypt(1, s))) == 0
+    assert K.decrypt(K.gate("mux", K.encrypt(0, s), K.encrypt(0, s), K.encrypt(1, s))) == 1
