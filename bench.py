@@ -203,9 +203,10 @@ def run_b200(args):
     from paper_2407_19871_b200 import ClientKeys, Context, TfheParams, _abi
 
     params = TfheParams(SECURITY)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream handle: the library launches on it and the
+    torch.cuda.set_stream(stream)  # CUDA events below are recorded on the same stream
     ctx = Context(params, local, stream=stream.cuda_stream)
-    G = GATES_PER_GPU
+    G = args.gates
     n1 = params.n + 1
 
     # ---- keys: generated once (client side) and broadcast over NVLink to every GPU
@@ -347,6 +348,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0,
                     help="seconds of CPU work per reference/cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gates", type=int, default=GATES_PER_GPU,
+                    help="gates per GPU (default: the cfg2 size; smaller only for profiling)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -124,6 +124,7 @@ template <class Bar>
 __device__ __forceinline__ void exch_p1_to_p2(double2 x[8], double2* buf, int t, Bar bar)
 {
     const int k = t >> 3, r = t & 7;
+    bar();  // the warp's previous reads of this single tile are done
 #pragma unroll
     for (int m = 0; m < 8; m++)
         buf[swz(64 * k + 8 * m + r)] = x[m];
@@ -135,6 +136,7 @@ __device__ __forceinline__ void exch_p1_to_p2(double2 x[8], double2* buf, int t,
 template <class Bar>
 __device__ __forceinline__ void exch_p2_to_p1(double2 x[8], double2* buf, int t, Bar bar)
 {
+    bar();  // the warp's previous reads of this single tile are done
 #pragma unroll
     for (int q = 0; q < 8; q++)
         buf[swz(8 * t + q)] = x[q];
@@ -159,9 +161,12 @@ __device__ __forceinline__ void exch_p1_to_p0(double2 x[8], double2* buf, int t,
 
 // Forward transform of the twisted input x (pass-0 layout) -> frequency slots
 // (pass-2 layout).  bufs: two 512-entry double2 tiles (double buffering).
-template <class Bar>
+// bufX: cross-warp exchange tile (needs the 64-thread barrier `bar`);
+// bufW: intra-warp exchange tile (after DIF stage 0 the two 256-point halves are
+// independent and warp w owns half w in passes 1 and 2, so `wbar` = __syncwarp).
+template <class Bar, class WBar>
 __device__ __forceinline__ void fft_forward(double2 x[8], const Twiddles& tw, double2* buf0,
-                                            double2* buf1, int t, Bar bar)
+                                            double2* buf1, int t, Bar bar, WBar wbar)
 {
     // pass 0: stages 0, 1, 2 (h = 256, 128, 64)
     dif(x[0], x[4], tw.p0a);
@@ -190,7 +195,7 @@ __device__ __forceinline__ void fft_forward(double2 x[8], const Twiddles& tw, do
     dif(x[2], x[3], tw.p1d);
     dif(x[4], x[5], tw.p1d);
     dif(x[6], x[7], tw.p1d);
-    exch_p1_to_p2(x, buf1, t, bar);
+    exch_p1_to_p2(x, buf1, t, wbar);
     // pass 2: stages 6, 7, 8 (h = 4, 2, 1) -- twiddles W[64 q], W[128 (q&1)], W[0]
     dif_1(x[0], x[4]);
     dif(x[1], x[5], tw.w64);
@@ -208,9 +213,9 @@ __device__ __forceinline__ void fft_forward(double2 x[8], const Twiddles& tw, do
 
 // Inverse transform (unscaled) of frequency slots (pass-2 layout) -> natural order
 // (pass-0 layout).  The 1/M scale lives in the untwist table.
-template <class Bar>
+template <class Bar, class WBar>
 __device__ __forceinline__ void fft_inverse(double2 x[8], const Twiddles& tw, double2* buf0,
-                                            double2* buf1, int t, Bar bar)
+                                            double2* buf1, int t, Bar bar, WBar wbar)
 {
     // pass 2^-1: stages 8, 7, 6
     dit_1(x[0], x[1]);
@@ -225,7 +230,7 @@ __device__ __forceinline__ void fft_inverse(double2 x[8], const Twiddles& tw, do
     dit(x[1], x[5], conj2(tw.w64));
     dit_mi(x[2], x[6]);
     dit(x[3], x[7], conj2(mul_i(tw.w64)));
-    exch_p2_to_p1(x, buf0, t, bar);
+    exch_p2_to_p1(x, buf1, t, wbar);
     // pass 1^-1: stages 5, 4, 3
     dit(x[0], x[1], conj2(tw.p1d));
     dit(x[2], x[3], conj2(tw.p1d));
@@ -239,7 +244,7 @@ __device__ __forceinline__ void fft_inverse(double2 x[8], const Twiddles& tw, do
     dit(x[1], x[5], conj2(tw.p1b));
     dit(x[2], x[6], conj2(mul_i(tw.p1a)));
     dit(x[3], x[7], conj2(mul_i(tw.p1b)));
-    exch_p1_to_p0(x, buf1, t, bar);
+    exch_p1_to_p0(x, buf0, t, bar);
     // pass 0^-1: stages 2, 1, 0
     dit(x[0], x[1], conj2(tw.p0d));
     dit(x[2], x[3], conj2(tw.p0d));

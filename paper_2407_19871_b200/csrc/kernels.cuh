@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
         x[q] = cmul(a, TW[j]);
     }
     auto bar = [] { __syncthreads(); };
-    fft_forward(x, tw, xbuf[0], xbuf[1], t, bar);
+    auto wbar = [] { __syncwarp(); };
+    fft_forward(x, tw, xbuf[0], xbuf[1], t, bar, wbar);
     double2* o = out + poly * FFT_M;
 #pragma unroll
     for (int q = 0; q < 8; q++)
@@ -90,6 +91,23 @@ __device__ __forceinline__ uint32_t rot_read(const uint32_t* p, uint32_t a, int 
     const uint32_t idx = (uint32_t)(j - (int)a) & 2047u;
     const uint32_t v = p[idx & 1023u];
     return idx < 1024u ? v : 0u - v;
+}
+
+// UT[j] = conj(TW[j]) / 512: scaling by a power of two is exact, so this equals the
+// oracle's untwist table bit for bit.
+__device__ __forceinline__ double2 untwist(double2 tw)
+{
+    return make_double2(tw.x * (1.0 / 512.0), -tw.y * (1.0 / 512.0));
+}
+
+// BK is streamed once per CTA per step: keep it out of L1 (it stays in L2).
+__device__ __forceinline__ double2 ld_stream(const double2* p)
+{
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p));
+    return v;
 }
 
 __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
@@ -110,11 +128,15 @@ __global__ void __launch_bounds__(64, 4)
                    const double2* __restrict__ TW, const double2* __restrict__ UT, uint32_t mu)
 {
     __shared__ uint32_t acc[2][1024];
-    __shared__ __align__(16) double2 xbuf[2][FFT_M];
-    __shared__ uint32_t abar[MAX_N + 1];
+    // exchange tiles: [0],[1] cross-warp (alternating), [2] intra-warp
+    __shared__ __align__(16) double2 xbuf[3][FFT_M];
+    __shared__ __align__(16) double2 tws[FFT_M];  // twist table psi^j
+    __shared__ uint16_t abar[MAX_N + 1];
 
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
+    for (int j = t; j < FFT_M; j += 64)
+        tws[j] = TW[j];
     const uint32_t n = dp.n;
 
     // ---- prologue: gate linear form (gate_engine.hpp:196-269) + mod switch to [0, 2N)
@@ -127,7 +149,7 @@ __global__ void __launch_bounds__(64, 4)
                 v += (uint32_t)it.c1 * a1[i];
             if (i == n)
                 v += it.off;
-            abar[i] = (v + (1u << 20)) >> 21;  // round(v * 2N / 2^32), N = 1024
+            abar[i] = (uint16_t)((v + (1u << 20)) >> 21);  // round(v * 2N / 2^32), N = 1024
         }
     }
     __syncthreads();
@@ -142,6 +164,8 @@ __global__ void __launch_bounds__(64, 4)
     }
     const Twiddles tw = load_twiddles(W, t);
     auto bar = [] { __syncthreads(); };
+    auto wbar = [] { __syncwarp(); };
+    int xs = 0;  // alternating cross-warp tile
 
     constexpr uint32_t HALF = 1u << (BGBIT - 1);
     constexpr uint32_t MASK = (1u << BGBIT) - 1;
@@ -175,39 +199,47 @@ __global__ void __launch_bounds__(64, 4)
             }
 #pragma unroll 1
             for (int p = 0; p < L; p++) {
+                // prefetch this row's BK slots; the loads land while the FFT runs
+                const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
+                double2 BA[8], BB[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    BA[q] = ld_stream(row + q * 64 + t);
+                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
+                }
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     const int dlo = (int)((tmp[q] >> sh) & MASK) - (int)HALF;
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
-                    x[q] = cmul(make_double2((double)dlo, (double)dhi), TW[t + 64 * q]);
+                    x[q] = cmul(make_double2((double)dlo, (double)dhi), tws[t + 64 * q]);
                 }
-                fft_forward(x, tw, xbuf[0], xbuf[1], t, bar);
-                const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
+                fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+                xs ^= 1;
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
-                    const double2 BA = row[q * 64 + t];
-                    const double2 BB = row[FFT_M + q * 64 + t];
-                    mac(oA[q], x[q], BA);
-                    mac(oB[q], x[q], BB);
+                    mac(oA[q], x[q], BA[q]);
+                    mac(oB[q], x[q], BB[q]);
                 }
             }
         }
         // inverse transforms, round, accumulate into ACC
-        fft_inverse(oA, tw, xbuf[0], xbuf[1], t, bar);
+        fft_inverse(oA, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+        xs ^= 1;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
-            const double2 w = cmul(oA[q], UT[j]);
+            const double2 w = cmul(oA[q], untwist(tws[j]));
             acc[0][j] += (uint32_t)__double2ll_rn(w.x);
             acc[0][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
-        fft_inverse(oB, tw, xbuf[0], xbuf[1], t, bar);
+        fft_inverse(oB, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+        xs ^= 1;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
-            const double2 w = cmul(oB[q], UT[j]);
+            const double2 w = cmul(oB[q], untwist(tws[j]));
             acc[1][j] += (uint32_t)__double2ll_rn(w.x);
             acc[1][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
@@ -222,19 +254,23 @@ __global__ void __launch_bounds__(64, 4)
 }
 
 // ---------------------------------------------------------------------------
-// K2: key switching.  CT ciphertexts per CTA share every KSK row load; each
-// thread owns two output columns.  Digits (t = 8 digits of basebit = 2) of the
-// combined N-dim mask are staged in shared memory as one u16 per coefficient.
+// K2: key switching.  KS_CT ciphertexts per CTA share every KSK row load; each
+// thread owns KS_COLS consecutive output columns (one 16-byte load per row).
+// The 2-bit digits (t = 8, basebit = 2) of the combined N-dim mask are staged in
+// shared memory, one u16 per coefficient; a digit is the same for every lane of a
+// warp (all lanes work on the same ciphertext), so the row choice is a
+// warp-uniform branch and each selected row costs one add per column.
 // ---------------------------------------------------------------------------
-constexpr int KS_CT = 32;
-constexpr int KS_THREADS = 320;  // 640 columns >= n_stride
+constexpr int KS_CT = 16;
+constexpr int KS_COLS = 4;
+constexpr int KS_THREADS = 160;  // 640 columns >= n_stride
 
-__global__ void __launch_bounds__(KS_THREADS, 1)
+__global__ void __launch_bounds__(KS_THREADS, 2)
     k_keyswitch(DevParams dp, const KsItem* __restrict__ items, uint32_t count,
                 const uint32_t* __restrict__ pool_N, uint32_t* __restrict__ pool_n,
                 const uint32_t* __restrict__ ksk)
 {
-    extern __shared__ uint16_t dig[];  // [KS_CT][N]
+    extern __shared__ uint16_t dig[];  // [N][KS_CT]
     __shared__ uint32_t body[KS_CT];
     const uint32_t N = dp.N;
     const uint32_t first = blockIdx.x * KS_CT;
@@ -251,7 +287,7 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
                 v += pool_N[(size_t)it.in1 * dp.N_stride + i];
             d = (uint16_t)((v + prec) >> 16);
         }
-        dig[e] = d;
+        dig[i * KS_CT + c] = d;
     }
     if (threadIdx.x < KS_CT) {
         uint32_t b = 0;
@@ -265,46 +301,50 @@ __global__ void __launch_bounds__(KS_THREADS, 1)
     }
     __syncthreads();
 
-    const uint32_t col = threadIdx.x * 2;
-    const bool active = col < dp.n_stride;
-    uint32_t acc0[KS_CT], acc1[KS_CT];
+    const uint32_t col = threadIdx.x * KS_COLS;
+    if (col >= dp.n_stride)
+        return;
+    uint4 acc[KS_CT];
 #pragma unroll
     for (int c = 0; c < KS_CT; c++) {
-        acc0[c] = (col == dp.n) ? body[c] : 0u;
-        acc1[c] = (col + 1 == dp.n) ? body[c] : 0u;
+        acc[c] = make_uint4(0u, 0u, 0u, 0u);
+        if (col + 0 == dp.n) acc[c].x = body[c];
+        if (col + 1 == dp.n) acc[c].y = body[c];
+        if (col + 2 == dp.n) acc[c].z = body[c];
+        if (col + 3 == dp.n) acc[c].w = body[c];
     }
     const size_t row_stride = dp.n_stride;
-    if (active) {
-        for (uint32_t i = 0; i < N; i++) {
-            uint2 rows[8][3];
-            const uint32_t* base = ksk + (size_t)i * 8 * 3 * row_stride + col;
+    const uint4* base = reinterpret_cast<const uint4*>(ksk + col);
+    const size_t rs4 = row_stride / 4;
+    for (uint32_t i = 0; i < N; i++) {
+        uint32_t dw[KS_CT / 2];
+        const uint32_t* dp32 = reinterpret_cast<const uint32_t*>(dig + i * KS_CT);
 #pragma unroll
-            for (int j = 0; j < 8; j++)
+        for (int c = 0; c < KS_CT / 2; c++)
+            dw[c] = dp32[c];  // broadcast: two ciphertexts' digit words
 #pragma unroll
-                for (int d = 0; d < 3; d++)
-                    rows[j][d] = __ldg(reinterpret_cast<const uint2*>(base + (j * 3 + d) * row_stride));
+        for (int j = 0; j < 8; j++) {
+            const uint4* rj = base + ((size_t)i * 24 + j * 3) * rs4;
+            const uint4 r1 = __ldg(rj), r2 = __ldg(rj + rs4), r3 = __ldg(rj + 2 * rs4);
 #pragma unroll
             for (int c = 0; c < KS_CT; c++) {
-                const uint32_t dw = dig[c * N + i];
-#pragma unroll
-                for (int j = 0; j < 8; j++) {
-                    const uint32_t d = (dw >> (14 - 2 * j)) & 3u;
-                    uint32_t s0 = d == 1 ? rows[j][0].x : (d == 2 ? rows[j][1].x : rows[j][2].x);
-                    uint32_t s1 = d == 1 ? rows[j][0].y : (d == 2 ? rows[j][1].y : rows[j][2].y);
-                    s0 = d ? s0 : 0u;
-                    s1 = d ? s1 : 0u;
-                    acc0[c] -= s0;
-                    acc1[c] -= s1;
+                const uint32_t w = dw[c >> 1] >> ((c & 1) * 16);
+                const uint32_t d = (w >> (14 - 2 * j)) & 3u;
+                if (d == 1) {
+                    acc[c].x -= r1.x; acc[c].y -= r1.y; acc[c].z -= r1.z; acc[c].w -= r1.w;
+                } else if (d == 2) {
+                    acc[c].x -= r2.x; acc[c].y -= r2.y; acc[c].z -= r2.z; acc[c].w -= r2.w;
+                } else if (d == 3) {
+                    acc[c].x -= r3.x; acc[c].y -= r3.y; acc[c].z -= r3.z; acc[c].w -= r3.w;
                 }
             }
         }
+    }
 #pragma unroll
-        for (int c = 0; c < KS_CT; c++) {
-            if ((uint32_t)c < nct) {
-                const KsItem it = items[first + c];
-                uint32_t* o = pool_n + (size_t)it.out * dp.n_stride + col;
-                *reinterpret_cast<uint2*>(o) = make_uint2(acc0[c], acc1[c]);
-            }
+    for (int c = 0; c < KS_CT; c++) {
+        if ((uint32_t)c < nct) {
+            const KsItem it = items[first + c];
+            *reinterpret_cast<uint4*>(pool_n + (size_t)it.out * dp.n_stride + col) = acc[c];
         }
     }
 }
