@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblocpir_b200.so")
+# LOCPIR_B200_LIB selects an alternative in-tree build (A/B experiments)
+LIB_PATH = os.environ.get("LOCPIR_B200_LIB") or os.path.join(HERE, "liblocpir_b200.so")
 
 OK, EINVAL, ELOGIC, ECUDA, ENOMEM = 0, -1, -2, -3, -4
 AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST = range(10)

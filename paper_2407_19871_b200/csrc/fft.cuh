@@ -80,9 +80,12 @@ __device__ __forceinline__ void dit_mi(double2& u, double2& v)  // conj(i) = -i
     u = cadd(u, tt);
 }
 
-// shared-memory swizzle: position 64k + 8m + r lives at 64k + 8m + (r ^ m); conflict-free
-// (one 128-byte wavefront per quarter warp) for all three register layouts.
-__device__ __forceinline__ int swz(int pos) { return (pos & ~7) | ((pos ^ (pos >> 3)) & 7); }
+// Exchange tile layout: position 64k + 8m + r (k, m, r in [0, 8)) lives at slot
+// 72k + 9m + r (576 slots).  Every register layout then addresses its 8 elements as
+// base + constant (72 q, 9 m or r), and each quarter warp (8 lanes x 16 B) hits 8
+// distinct 16-byte bank groups in all three layouts: conflict-free.
+constexpr int XTILE = 576;
+__device__ __forceinline__ int slot_of(int k, int m, int r) { return 72 * k + 9 * m + r; }
 
 // Per-thread twiddles, constant for the whole kernel.
 struct Twiddles {
@@ -107,56 +110,62 @@ __device__ __forceinline__ Twiddles load_twiddles(const double2* __restrict__ W,
     return tw;
 }
 
-// Exchange helpers.  `bar` synchronises the 64 threads owning the polynomial.
+// Exchange helpers.  `bar` synchronises the threads that share the tile.
+// pass-0 layout: thread t = 8m + r holds k = q;  pass-1: t = 8k + r holds m;
+// pass-2: t = 8k + m holds r.
 template <class Bar>
 __device__ __forceinline__ void exch_p0_to_p1(double2 x[8], double2* buf, int t, Bar bar)
 {
+    double2* w = buf + slot_of(0, t >> 3, t & 7);
 #pragma unroll
     for (int q = 0; q < 8; q++)
-        buf[swz(t + 64 * q)] = x[q];
+        w[72 * q] = x[q];
     bar();
-    const int k = t >> 3, r = t & 7;
+    const double2* rd = buf + slot_of(t >> 3, 0, t & 7);
 #pragma unroll
     for (int m = 0; m < 8; m++)
-        x[m] = buf[swz(64 * k + 8 * m + r)];
+        x[m] = rd[9 * m];
 }
 template <class Bar>
 __device__ __forceinline__ void exch_p1_to_p2(double2 x[8], double2* buf, int t, Bar bar)
 {
-    const int k = t >> 3, r = t & 7;
     bar();  // the warp's previous reads of this single tile are done
+    double2* w = buf + slot_of(t >> 3, 0, t & 7);
 #pragma unroll
     for (int m = 0; m < 8; m++)
-        buf[swz(64 * k + 8 * m + r)] = x[m];
+        w[9 * m] = x[m];
     bar();
+    const double2* rd = buf + slot_of(t >> 3, t & 7, 0);
 #pragma unroll
     for (int q = 0; q < 8; q++)
-        x[q] = buf[swz(8 * t + q)];
+        x[q] = rd[q];
 }
 template <class Bar>
 __device__ __forceinline__ void exch_p2_to_p1(double2 x[8], double2* buf, int t, Bar bar)
 {
     bar();  // the warp's previous reads of this single tile are done
+    double2* w = buf + slot_of(t >> 3, t & 7, 0);
 #pragma unroll
     for (int q = 0; q < 8; q++)
-        buf[swz(8 * t + q)] = x[q];
+        w[q] = x[q];
     bar();
-    const int k = t >> 3, r = t & 7;
+    const double2* rd = buf + slot_of(t >> 3, 0, t & 7);
 #pragma unroll
     for (int m = 0; m < 8; m++)
-        x[m] = buf[swz(64 * k + 8 * m + r)];
+        x[m] = rd[9 * m];
 }
 template <class Bar>
 __device__ __forceinline__ void exch_p1_to_p0(double2 x[8], double2* buf, int t, Bar bar)
 {
-    const int k = t >> 3, r = t & 7;
+    double2* w = buf + slot_of(t >> 3, 0, t & 7);
 #pragma unroll
     for (int m = 0; m < 8; m++)
-        buf[swz(64 * k + 8 * m + r)] = x[m];
+        w[9 * m] = x[m];
     bar();
+    const double2* rd = buf + slot_of(0, t >> 3, t & 7);
 #pragma unroll
     for (int q = 0; q < 8; q++)
-        x[q] = buf[swz(t + 64 * q)];
+        x[q] = rd[72 * q];
 }
 
 // Forward transform of the twisted input x (pass-0 layout) -> frequency slots

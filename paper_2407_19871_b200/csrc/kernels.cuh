@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
                                                    const double2* __restrict__ W,
                                                    const double2* __restrict__ TW)
 {
-    __shared__ __align__(16) double2 xbuf[2][FFT_M];
+    __shared__ __align__(16) double2 xbuf[2][XTILE];
     const int t = threadIdx.x;
     const size_t poly = blockIdx.x;
     const uint32_t* b = bk + poly * 1024;
@@ -84,6 +84,12 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
 // K1: blind rotation + sample extraction, one 64-thread CTA per ciphertext.
 // ---------------------------------------------------------------------------
 constexpr int MAX_N = 1023;
+#ifndef TWIST_REGS
+#define TWIST_REGS 0
+#endif
+#ifndef BR_MIN_BLOCKS
+#define BR_MIN_BLOCKS 4
+#endif
 
 __device__ __forceinline__ uint32_t rot_read(const uint32_t* p, uint32_t a, int j)
 {
@@ -121,7 +127,7 @@ __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
 }
 
 template <int L, int BGBIT>
-__global__ void __launch_bounds__(64, 4)
+__global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     k_blind_rotate(DevParams dp, const BrItem* __restrict__ items,
                    const uint32_t* __restrict__ pool_n, uint32_t* __restrict__ pool_N,
                    const double2* __restrict__ bkf, const double2* __restrict__ W,
@@ -129,14 +135,25 @@ __global__ void __launch_bounds__(64, 4)
 {
     __shared__ uint32_t acc[2][1024];
     // exchange tiles: [0],[1] cross-warp (alternating), [2] intra-warp
-    __shared__ __align__(16) double2 xbuf[3][FFT_M];
-    __shared__ __align__(16) double2 tws[FFT_M];  // twist table psi^j
+    __shared__ __align__(16) double2 xbuf[3][XTILE];
     __shared__ uint16_t abar[MAX_N + 1];
+#if !TWIST_REGS
+    __shared__ __align__(16) double2 tws[FFT_M];  // twist table psi^j
+#endif
 
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
+#if TWIST_REGS
+    double2 twr[8];  // this thread's twist factors psi^j, j = t + 64 q (untwist = conj / 512)
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+        twr[q] = TW[t + 64 * q];
+#define TWIST(q) twr[q]
+#else
     for (int j = t; j < FFT_M; j += 64)
         tws[j] = TW[j];
+#define TWIST(q) tws[t + 64 * (q)]
+#endif
     const uint32_t n = dp.n;
 
     // ---- prologue: gate linear form (gate_engine.hpp:196-269) + mod switch to [0, 2N)
@@ -213,7 +230,7 @@ __global__ void __launch_bounds__(64, 4)
                 for (int q = 0; q < 8; q++) {
                     const int dlo = (int)((tmp[q] >> sh) & MASK) - (int)HALF;
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
-                    x[q] = cmul(make_double2((double)dlo, (double)dhi), tws[t + 64 * q]);
+                    x[q] = cmul(make_double2((double)dlo, (double)dhi), TWIST(q));
                 }
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
@@ -230,7 +247,7 @@ __global__ void __launch_bounds__(64, 4)
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
-            const double2 w = cmul(oA[q], untwist(tws[j]));
+            const double2 w = cmul(oA[q], untwist(TWIST(q)));
             acc[0][j] += (uint32_t)__double2ll_rn(w.x);
             acc[0][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
@@ -239,7 +256,7 @@ __global__ void __launch_bounds__(64, 4)
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
-            const double2 w = cmul(oB[q], untwist(tws[j]));
+            const double2 w = cmul(oB[q], untwist(TWIST(q)));
             acc[1][j] += (uint32_t)__double2ll_rn(w.x);
             acc[1][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }

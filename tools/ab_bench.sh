@@ -1,0 +1,15 @@
+# A/B: bench each variant library given as arguments (names of paper_2407_19871_b200/lib_<v>.so)
+echo "" > gpurun_out/ab.txt
+for v in base "$@"; do
+  if [ "$v" = base ]; then lib=""; else lib=paper_2407_19871_b200/lib_$v.so; fi
+  LOCPIR_B200_LIB=$lib timeout 300 python bench.py --steps 3 --warmup 1 --no-cpu-baseline > gpurun_out/ab_$v.log 2>&1
+  python - "$v" <<'PY' >> gpurun_out/ab.txt
+import json, sys
+v = sys.argv[1]
+try:
+    d = json.loads(open(f'gpurun_out/ab_{v}.log').read().strip().splitlines()[-1])
+    print('%-10s value %.0f ms/step %.1f br_ms %.1f frac %.3f ks_ms %.1f e2e %.0f correct %s' % (v, d['value'], d['ms_per_step'], d['roofline']['avg_launch_ms'], d['roofline']['frac'], d['keyswitch']['avg_launch_ms'], d['e2e']['value'], d['correct']))
+except Exception as e:
+    print(v, 'FAILED', e)
+PY
+done
