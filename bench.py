@@ -210,19 +210,9 @@ def run_b200(args):
     n1 = params.n + 1
 
     # ---- keys: generated once (client side) and broadcast over NVLink to every GPU
+    from paper_2407_19871_b200.dist import broadcast_keys, max_over_ranks as _mor
     t_setup = time.perf_counter()
-    bk_t = torch.empty(params.bk_words(), dtype=torch.int32, device="cuda")
-    ksk_t = torch.empty(params.ksk_words(), dtype=torch.int32, device="cuda")
-    if rank == 0:
-        keys = ClientKeys(params, KEY_SEED)
-        bk_t.copy_(torch.from_numpy(keys.bk.view(np.int32)))
-        ksk_t.copy_(torch.from_numpy(keys.ksk.view(np.int32)))
-    else:
-        keys = ClientKeys(params, KEY_SEED, evaluation_keys=False)
-    if ws > 1:
-        import torch.distributed as dist
-        dist.broadcast(bk_t, src=0)
-        dist.broadcast(ksk_t, src=0)
+    keys, bk_t, ksk_t = broadcast_keys(params, KEY_SEED, rank, device="cuda")
     torch.cuda.synchronize()
     ctx.upload_keys(bk_t.data_ptr(), ksk_t.data_ptr(), on_device=True)
     del bk_t, ksk_t
@@ -245,12 +235,7 @@ def run_b200(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if ws == 1:
-            return x
-        import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _mor(x, device="cuda")
 
     # ---- device-resident throughput (value)
     for _ in range(args.warmup):

@@ -1,0 +1,174 @@
+// test_mirror.cpp -- the reference's own engine/circuit tests, restated against the
+// C++ mirror (paper_2407_19871_b200/host/locpir_b200.hpp) of the B200 engine.
+// Mirrors test_gate_engine.cpp:17-97 and test_circuits.cpp:26-213 (Catch2 is not in
+// this image; a tiny CHECK macro stands in).  Driven by tests/test_cpp_mirror.py.
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <stdexcept>
+
+#include "../../paper_2407_19871_b200/host/locpir_b200.hpp"
+
+using namespace locpir_b200;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(x)                                                                   \
+    do {                                                                           \
+        g_checks++;                                                                \
+        if (!(x)) {                                                                \
+            g_fail++;                                                              \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #x); \
+        }                                                                          \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)                  \
+    do {                                          \
+        bool thrown_ = false;                     \
+        try {                                     \
+            (void)(expr);                         \
+        } catch (const T&) {                      \
+            thrown_ = true;                       \
+        }                                         \
+        CHECK(thrown_);                           \
+    } while (0)
+
+static CipherWord enc_int(int64_t v, int l, GateEngine& e)
+{
+    std::vector<uint8_t> bits(l);
+    const uint64_t u = static_cast<uint64_t>(v);
+    for (int i = 0; i < l; i++)
+        bits[i] = (u >> i) & 1;
+    return {e.encrypt_many(bits)};
+}
+
+static CipherWord const_int(int64_t v, int l, GateEngine& e)
+{
+    CipherWord w;
+    BatchScope s(e);
+    const uint64_t u = static_cast<uint64_t>(v);
+    for (int i = 0; i < l; i++)
+        w.bits.push_back(e.constant((u >> i) & 1));
+    return w;
+}
+
+static uint64_t dec_service(const ServiceCiphertext& s, GateEngine& e)
+{
+    uint64_t v = 0;
+    for (size_t j = 0; j < s.bits.size(); j++)
+        if (e.decrypt(s.bits[j]))
+            v |= 1ull << j;
+    return v;
+}
+
+int main()
+{
+    const ClientKeys keys(Params::tfhe80(), 42);
+    GateEngine eng = GateEngine::make_b200(keys, 43);
+
+    // test_gate_engine.cpp:17-38 truth tables
+    for (int a = 0; a <= 1; a++)
+        for (int b = 0; b <= 1; b++) {
+            const CipherBit ca = eng.encrypt(a), cb = eng.encrypt(b);
+            CHECK(eng.decrypt(eng.hom_and(ca, cb)) == (a && b));
+            CHECK(eng.decrypt(eng.hom_or(ca, cb)) == (a || b));
+            CHECK(eng.decrypt(eng.hom_xor(ca, cb)) == (a != b));
+            CHECK(eng.decrypt(eng.hom_xnor(ca, cb)) == (a == b));
+            CHECK(eng.decrypt(eng.hom_nand(ca, cb)) == !(a && b));
+            CHECK(eng.decrypt(eng.hom_not(ca)) == !a);
+            for (int s = 0; s <= 1; s++) {
+                const CipherBit cs = eng.encrypt(s);
+                CHECK(eng.decrypt(eng.hom_mux(cs, ca, cb)) == (s ? a : b));
+            }
+        }
+
+    // test_gate_engine.cpp:40-69 counters
+    {
+        eng.reset_counters();
+        const CipherBit a = eng.encrypt(true), b = eng.encrypt(false);
+        (void)eng.hom_and(a, b);
+        (void)eng.hom_or(a, b);
+        (void)eng.hom_or(a, b);
+        (void)eng.hom_xor(a, b);
+        (void)eng.hom_xnor(a, b);
+        (void)eng.hom_not(a);
+        (void)eng.hom_mux(a, a, b);
+        (void)eng.constant(true);
+        const GateCounterSnapshot s = eng.counters();
+        CHECK(s.and_gates == 1 && s.or_gates == 2 && s.xor_gates == 1 && s.xnor_gates == 1);
+        CHECK(s.not_gates == 1 && s.mux_gates == 1);
+        CHECK(s.bootstrap_units() == 1 + 2 + 1 + 1 + 2 * 1);
+        CHECK(s.as_map().at("bootstrap_units") == s.bootstrap_units());
+    }
+
+    // test_gate_engine.cpp:140-155 errors
+    {
+        GateEngine other = GateEngine::make_b200(keys, 44);
+        const CipherBit mine = eng.encrypt(true);
+        CHECK_THROWS_AS(other.hom_and(mine, mine), std::invalid_argument);
+        CHECK(parse_engine_kind("tfhe-b200") == EngineKind::TfheB200);
+        CHECK_THROWS_AS(parse_engine_kind("tfhe"), std::invalid_argument);
+    }
+
+    // test_circuits.cpp:26-40 comparator vs signed order at l = 6 (batched per pair set)
+    {
+        const int l = 6;
+        const int64_t vals[] = {-32, -17, -1, 0, 1, 17, 31};
+        std::vector<std::tuple<int64_t, int64_t, CipherBit, CipherBit>> res;
+        {
+            std::vector<std::pair<CipherWord, CipherWord>> words;
+            for (int64_t a : vals)
+                for (int64_t b : vals)
+                    words.push_back({enc_int(a, l, eng), enc_int(b, l, eng)});
+            BatchScope scope(eng);
+            size_t k = 0;
+            for (int64_t a : vals)
+                for (int64_t b : vals) {
+                    const auto& w = words[k++];
+                    res.emplace_back(a, b, hom_less(w.first, w.second, eng),
+                                     hom_less_equal(w.first, w.second, eng));
+                }
+        }
+        for (auto& [a, b, lt, le] : res) {
+            CHECK(eng.decrypt(lt) == (a < b));
+            CHECK(eng.decrypt(le) == (a <= b));
+        }
+    }
+
+    // test_circuits.cpp:150-213 loc_pir retrieval, half-open edges, counts
+    {
+        const int l = 6;
+        auto regions_for = [&]() {
+            std::vector<EncodedRegion> r(3);
+            BatchScope s(eng);
+            const int64_t spec[3][4] = {{0, 8, 0, 8}, {8, 16, 0, 8}, {-16, -4, -12, -4}};
+            const uint64_t svc[3] = {5, 3, 7};
+            for (int i = 0; i < 3; i++) {
+                r[i].x1 = const_int(spec[i][0], l, eng);
+                r[i].x2 = const_int(spec[i][1], l, eng);
+                r[i].y1 = const_int(spec[i][2], l, eng);
+                r[i].y2 = const_int(spec[i][3], l, eng);
+                for (int j = 0; j < 3; j++)
+                    r[i].service.bits.push_back(eng.constant((svc[i] >> j) & 1));
+                r[i].region_id = i;
+            }
+            return r;
+        };
+        const auto regions = regions_for();
+        const std::pair<std::pair<int64_t, int64_t>, uint64_t> cases[] = {
+            {{5, 2}, 5}, {{9, 1}, 3}, {{-10, -6}, 7}, {{28, 28}, 0},
+            {{0, 0}, 5}, {{8, 0}, 3}, {{16, 0}, 0},   {{5, 8}, 0}};
+        eng.reset_counters();
+        for (bool tree : {false, true})
+            for (const auto& [pt, want] : cases) {
+                const CipherWord x = enc_int(pt.first, l, eng), y = enc_int(pt.second, l, eng);
+                CHECK(dec_service(loc_pir(x, y, regions, eng, tree), eng) == want);
+            }
+        const GateCounterSnapshot s = eng.counters();
+        const uint64_t q = 16, N = 3, m = 3;
+        CHECK(s.xnor_gates == q * N * 4 * l && s.mux_gates == q * N * 4 * l);
+        CHECK(s.and_gates == q * N * (3 + m) && s.xor_gates == q * N * m);
+        CHECK(s.bootstrap_units() == q * N * (12 * l + 2 * m + 3));
+    }
+
+    std::printf("%d checks, %d failed\n", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+}

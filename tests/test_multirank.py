@@ -1,0 +1,71 @@
+"""World-size-2 gloo test of the multi-GPU host path (paper_2407_19871_b200/dist.py):
+key broadcast from rank 0, static sharding, per-rank gate evaluation, gather to rank 0.
+No GPU: each rank evaluates its shard with the CPU oracle standing in for its GPU, so
+this checks the plumbing the NCCL path uses."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_19871_b200 import TfheParams
+    from paper_2407_19871_b200.dist import broadcast_keys, gather_to_root, max_over_ranks, shard_range
+    from oracle import oracle as O
+    p = TfheParams(80)
+    keys, bk, ksk = broadcast_keys(p, seed=7, rank=rank)
+    # every rank received the same evaluation keys the oracle derives from the seed
+    ok = O.TfheKeys(80, 7)
+    assert np.array_equal(bk.numpy().view(np.uint32), ok.bk())
+    assert np.array_equal(ksk.numpy().view(np.uint32), ok.ksk())
+    assert np.array_equal(keys.lwe_key, ok.lwe_key)
+    total = 5
+    A = np.array([0, 1, 1, 0, 1], np.uint8)
+    B = np.array([1, 1, 0, 0, 1], np.uint8)
+    a = keys.encrypt_bits(A, 11)   # the client's full batch (same seed on every rank)
+    b = keys.encrypt_bits(B, 12)
+    lo, hi = shard_range(total, rank, world)
+    out = ok.gate_batch("nand", a[lo:hi], b[lo:hi]) if hi > lo else np.zeros((0, p.n + 1), np.uint32)
+    full = gather_to_root(torch.from_numpy(out.view(np.int32)), total, rank, world)
+    t = max_over_ranks(float(rank + 1))
+    if rank == 0:
+        got = keys.decrypt_bits(full.numpy().view(np.uint32))
+        np.save(os.path.join(outdir, "got.npy"), got)
+        np.save(os.path.join(outdir, "t.npy"), np.array([t]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_range_partitions():
+    from paper_2407_19871_b200.dist import shard_range
+    for total in (0, 1, 7, 65536):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(total, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == total
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+
+
+def test_two_rank_gloo_sharded_gates(tmp_path):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    got = np.load(tmp_path / "got.npy")
+    assert list(got) == [1, 0, 1, 1, 0]  # NAND
+    assert float(np.load(tmp_path / "t.npy")[0]) == 2.0  # max over ranks
