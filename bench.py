@@ -193,6 +193,65 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+LOCPIR_SAMPLES = {  # name: queries timed per rank (a bounded sample of the config's batch)
+    "cfg1": 1, "cfg3": 1, "cfg4": 256, "cfg5": 8,
+}
+
+
+def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
+    """LocPIR queries/s for BASELINE.json configs 0, 2, 3, 4 through the batched loc_pir
+    program (level-scheduled).  Each rank runs its own shard of queries (cfg4/cfg5:
+    queries sharded; cfg1/cfg3: replicas).  Decrypted results are checked against the
+    plaintext XOR of the payloads of all containing boxes."""
+    import torch
+    from paper_2407_19871_b200 import ClientKeys, Context, TfheParams, workloads as W
+    out = {}
+    ctx80 = keys80 = None
+    for name, (sec, Qfull, R, l, m, enc) in W.CONFIGS.items():
+        if sec == 80:
+            if ctx80 is None:
+                p80 = TfheParams(80)
+                keys80 = ClientKeys(p80, KEY_SEED)
+                ctx80 = Context(p80, local, stream=torch.cuda.current_stream().cuda_stream)
+                ctx80.upload_keys(keys80.bk, keys80.ksk)
+            ctx, keys = ctx80, keys80
+        else:
+            ctx, keys = ctx128, keys128
+        Q = min(Qfull, LOCPIR_SAMPLES[name])
+        b = W.make_batch(Q, R, l, m, seed=KEY_SEED + 17 * rank + len(out), encrypted_bounds=enc)
+        lay = W.PoolLayout(b)
+        ctx.pool_reserve(lay.total)
+        W.load_batch(ctx, keys, b, lay, seed=5000 + rank)
+        prog = W.program(ctx, b, lay)
+        prog.launch()  # warm-up
+        torch.cuda.synchronize()
+        reps = 3 if b.units() < 200000 else 1
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            prog.launch()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+        ok = bool(np.array_equal(W.read_results(ctx, keys, b, lay), b.truth()))
+        out[name] = {
+            "queries_per_s": ws * Q / (ms / 1e3), "ms_per_batch": ms, "queries_per_gpu": Q,
+            "full_batch_queries": Qfull, "boxes": R, "l": l, "m": m, "security_bits": sec,
+            "encrypted_boundaries": enc, "bootstrap_units_per_query": b.units() // Q,
+            "levels_launched": prog.kernels, "units_per_s": ws * b.units() / (ms / 1e3),
+            "correct": ok,
+            "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
+                                                       "(per-query cost is batch-independent "
+                                                       "once the GPU is saturated)",
+        }
+        prog.close()
+    if ctx80 is not None:
+        ctx80.close()
+    return out
+
+
+# ---------------------------------------------------------------------------
 def run_b200(args):
     import torch
     ws, rank, local = dist_env()
@@ -286,6 +345,8 @@ def run_b200(args):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     e2e_ok = bool(np.array_equal(keys.decrypt_bits(o_h.numpy().view(np.uint32)), 1 - (A & B)))
 
+    locpir_results = None if args.no_locpir else run_locpir_suite(args, ctx, keys, ws, rank,
+                                                                   local, max_over_ranks)
     if rank == 0:
         line = {
             "metric": "bootstrapped gates/s (128-bit TFHE)", "value": value, "unit": "gates/s",
@@ -312,6 +373,8 @@ def run_b200(args):
             "clocks": clk,
             "setup_s": setup_s,
         }
+        if not args.no_locpir:
+            line["locpir"] = locpir_results
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_oracle_rate(budget_s=args.ref_budget)
             line["reference_standin"] = standin_rate()
@@ -333,6 +396,8 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=12.0,
                     help="seconds of CPU work per reference/cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-locpir", action="store_true",
+                    help="skip the LocPIR queries/s measurements (configs 0, 2, 3, 4)")
     ap.add_argument("--gates", type=int, default=GATES_PER_GPU,
                     help="gates per GPU (default: the cfg2 size; smaller only for profiling)")
     args = ap.parse_args()

@@ -87,6 +87,9 @@ constexpr int MAX_N = 1023;
 #ifndef TWIST_REGS
 #define TWIST_REGS 0
 #endif
+#ifndef BK_PREFETCH
+#define BK_PREFETCH 2
+#endif
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4
 #endif
@@ -219,11 +222,16 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 // prefetch this row's BK slots; the loads land while the FFT runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
                 double2 BA[8], BB[8];
+#if BK_PREFETCH >= 1
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
+                for (int q = 0; q < 8; q++)
                     BA[q] = ld_stream(row + q * 64 + t);
+#endif
+#if BK_PREFETCH >= 2
+#pragma unroll
+                for (int q = 0; q < 8; q++)
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
-                }
+#endif
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
 #pragma unroll
@@ -234,6 +242,16 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 }
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
+#if BK_PREFETCH < 2
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
+#endif
+#if BK_PREFETCH < 1
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    BA[q] = ld_stream(row + q * 64 + t);
+#endif
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     mac(oA[q], x[q], BA[q]);

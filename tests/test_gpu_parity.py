@@ -265,3 +265,28 @@ def test_errors_map_to_reference_exceptions(dev):
         e2.hom_and(a, a)  # cipher bit belongs to a different engine
     with pytest.raises(InvalidArgument):
         ctx.run([(_abi.AND, 0, 1, 0, ctx.pool_capacity + 5)])
+
+
+@pytest.mark.parametrize("name,Q,R", [("cfg1", 1, 1), ("cfg3", 1, 64), ("cfg4", 8, 16),
+                                       ("cfg5", 1, 4)])
+def test_locpir_config_shapes_match_plaintext(dev, name, Q, R):
+    """BASELINE.json configs 0/2/3/4 shapes (bounded batch sizes): the decrypted loc_pir
+    result equals the XOR of the payloads of all boxes containing the point, incl. the
+    encrypted-boundary l = 32 variant."""
+    from paper_2407_19871_b200 import workloads as W
+    sec, _, _, l, m, enc = W.CONFIGS[name]
+    p, keys, ctx = dev[sec]
+    b = W.make_batch(Q, R, l, m, seed=99 + R, encrypted_bounds=enc)
+    # make sure some queries land inside boxes: put query 0 at the centre of box 0
+    b.x[0] = (b.boxes[0, 0] + b.boxes[0, 1]) // 2
+    b.y[0] = (b.boxes[0, 2] + b.boxes[0, 3]) // 2
+    lay = W.PoolLayout(b)
+    ctx.pool_reserve(lay.total)
+    W.load_batch(ctx, keys, b, lay, seed=7)
+    ctx.counters_reset()
+    prog = W.program(ctx, b, lay)
+    prog.launch()
+    got = W.read_results(ctx, keys, b, lay)
+    assert np.array_equal(got, b.truth())
+    assert ctx.counters()["bootstrap_units"] == b.units()
+    prog.close()
