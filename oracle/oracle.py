@@ -31,7 +31,8 @@ class Params(C.Structure):
 class KeySet(C.Structure):
     _fields_ = [("p", Params), ("lwe_key", C.POINTER(C.c_uint8)),
                 ("trlwe_key", C.POINTER(C.c_uint8)), ("bk", C.POINTER(C.c_uint32)),
-                ("ksk", C.POINTER(C.c_uint32)), ("bk_fft", C.POINTER(C.c_double))]
+                ("ksk", C.POINTER(C.c_uint32)), ("bk_fft", C.POINTER(C.c_double)),
+                ("bk_fft_soa", C.POINTER(C.c_double))]
 
 
 class Sampler(C.Structure):

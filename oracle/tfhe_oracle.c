@@ -276,20 +276,29 @@ static const fft_tab* get_tab(uint32_t N)
     return t;
 }
 
-static void dif_forward(uint32_t M, cplx* z, const cplx* W)
+/* The transforms run on split re/im arrays (same per-element arithmetic as
+ * cmul/cadd/csub above; the layout only lets the compiler vectorize). */
+static void dif_forward_soa(uint32_t M, double* restrict zr, double* restrict zi,
+                            const cplx* W)
 {
     uint32_t s = 0;
     for (uint32_t h = M >> 1; h >= 1; h >>= 1, s++) {
         for (uint32_t b = 0; b < M; b += 2 * h)
             for (uint32_t j = 0; j < h; j++) {
-                cplx u = z[b + j], v = z[b + j + h];
-                z[b + j] = cadd(u, v);
-                z[b + j + h] = cmul(csub(u, v), W[j << s]);
+                const double ur = zr[b + j], ui = zi[b + j];
+                const double vr = zr[b + j + h], vi = zi[b + j + h];
+                const double wr = W[j << s].re, wi = W[j << s].im;
+                zr[b + j] = ur + vr;
+                zi[b + j] = ui + vi;
+                const double dr = ur - vr, di = ui - vi;
+                zr[b + j + h] = fma(dr, wr, -(di * wi));
+                zi[b + j + h] = fma(dr, wi, di * wr);
             }
     }
 }
 
-static void dit_inverse(uint32_t M, cplx* z, const cplx* W)
+static void dit_inverse_soa(uint32_t M, double* restrict zr, double* restrict zi,
+                            const cplx* W)
 {
     uint32_t logM = 0;
     while ((1u << logM) < M)
@@ -298,11 +307,44 @@ static void dit_inverse(uint32_t M, cplx* z, const cplx* W)
         uint32_t h = M >> (s + 1);
         for (uint32_t b = 0; b < M; b += 2 * h)
             for (uint32_t j = 0; j < h; j++) {
-                cplx u = z[b + j];
-                cplx v = cmul(z[b + j + h], cconj(W[j << s]));
-                z[b + j] = cadd(u, v);
-                z[b + j + h] = csub(u, v);
+                const double wr = W[j << s].re, wi = -W[j << s].im; /* conj(W) */
+                const double vr = zr[b + j + h], vi = zi[b + j + h];
+                const double tr = fma(vr, wr, -(vi * wi));
+                const double ti = fma(vr, wi, vi * wr);
+                const double ur = zr[b + j], ui = zi[b + j];
+                zr[b + j] = ur + tr;
+                zi[b + j] = ui + ti;
+                zr[b + j + h] = ur - tr;
+                zi[b + j + h] = ui - ti;
             }
+    }
+}
+
+static void dif_forward(uint32_t M, cplx* z, const cplx* W)
+{
+    double zr[1024], zi[1024];
+    for (uint32_t j = 0; j < M; j++) {
+        zr[j] = z[j].re;
+        zi[j] = z[j].im;
+    }
+    dif_forward_soa(M, zr, zi, W);
+    for (uint32_t j = 0; j < M; j++) {
+        z[j].re = zr[j];
+        z[j].im = zi[j];
+    }
+}
+
+static void dit_inverse(uint32_t M, cplx* z, const cplx* W)
+{
+    double zr[1024], zi[1024];
+    for (uint32_t j = 0; j < M; j++) {
+        zr[j] = z[j].re;
+        zi[j] = z[j].im;
+    }
+    dit_inverse_soa(M, zr, zi, W);
+    for (uint32_t j = 0; j < M; j++) {
+        z[j].re = zr[j];
+        z[j].im = zi[j];
     }
 }
 
@@ -407,7 +449,8 @@ int or_keyset_generate(or_keyset* ks, const or_params* p, uint64_t seed)
     ks->bk = (uint32_t*)malloc(sizeof(uint32_t) * or_bk_words(p));
     ks->ksk = (uint32_t*)malloc(sizeof(uint32_t) * or_ksk_words(p));
     ks->bk_fft = (double*)malloc(sizeof(double) * or_bk_words(p));
-    if (!ks->lwe_key || !ks->trlwe_key || !ks->bk || !ks->ksk || !ks->bk_fft)
+    ks->bk_fft_soa = (double*)malloc(sizeof(double) * or_bk_words(p));
+    if (!ks->lwe_key || !ks->trlwe_key || !ks->bk || !ks->ksk || !ks->bk_fft || !ks->bk_fft_soa)
         return -2;
 
     /* LWE key: the reference keygen (torus.hpp:146-154) */
@@ -466,6 +509,10 @@ int or_keyset_generate(or_keyset* ks, const or_params* p, uint64_t seed)
             for (uint32_t j = 0; j < N; j++)
                 tmp[j] = (int32_t)ks->bk[q * N + j];
             or_fft_forward_i32(N, tmp, ks->bk_fft + q * N);
+            for (uint32_t f = 0; f < N / 2; f++) {
+                ks->bk_fft_soa[q * N + f] = ks->bk_fft[q * N + 2 * f];
+                ks->bk_fft_soa[q * N + N / 2 + f] = ks->bk_fft[q * N + 2 * f + 1];
+            }
         }
         free(tmp);
     }
@@ -479,6 +526,7 @@ void or_keyset_free(or_keyset* ks)
     free(ks->bk);
     free(ks->ksk);
     free(ks->bk_fft);
+    free(ks->bk_fft_soa);
     memset(ks, 0, sizeof(*ks));
 }
 
@@ -519,31 +567,45 @@ int or_external_product(const or_keyset* ks, uint32_t i, const uint32_t* trlwe, 
                                          out + comp * N);
             }
     } else {
-        cplx* F = (cplx*)malloc(sizeof(cplx) * M);
-        cplx* acc = (cplx*)calloc(2 * M, sizeof(cplx));
+        const fft_tab* tab = get_tab(N);
+        double Fr[512], Fi[512], Ar[2][512], Ai[2][512];
+        memset(Ar, 0, sizeof(Ar));
+        memset(Ai, 0, sizeof(Ai));
         for (uint32_t c = 0; c < 2; c++)
             for (uint32_t q = 0; q < p->l; q++) {
                 or_decompose(p, trlwe + c * N, q, dig);
-                or_fft_forward_i32(N, dig, (double*)F);
+                for (uint32_t j = 0; j < M; j++) {  /* twist = cmul((d_j, d_{j+M}), TW[j]) */
+                    const double ar = (double)dig[j], ai = (double)dig[j + M];
+                    Fr[j] = fma(ar, tab->TW[j].re, -(ai * tab->TW[j].im));
+                    Fi[j] = fma(ar, tab->TW[j].im, ai * tab->TW[j].re);
+                }
+                dif_forward_soa(M, Fr, Fi, tab->W);
                 const uint32_t r = c * p->l + q;
                 for (uint32_t comp = 0; comp < 2; comp++) {
-                    const cplx* B =
-                        (const cplx*)(ks->bk_fft + (((size_t)i * rows + r) * 2 + comp) * N);
-                    cplx* a = acc + comp * M;
+                    const double* Br = ks->bk_fft_soa + (((size_t)i * rows + r) * 2 + comp) * N;
+                    const double* Bi = Br + M;
+                    double* ar = Ar[comp];
+                    double* ai = Ai[comp];
                     for (uint32_t f = 0; f < M; f++) {
-                        double re = fma(F[f].re, B[f].re, a[f].re);
-                        re = fma(-F[f].im, B[f].im, re);
-                        double im = fma(F[f].re, B[f].im, a[f].im);
-                        im = fma(F[f].im, B[f].re, im);
-                        a[f].re = re;
-                        a[f].im = im;
+                        double re = fma(Fr[f], Br[f], ar[f]);
+                        re = fma(-Fi[f], Bi[f], re);
+                        double im = fma(Fr[f], Bi[f], ai[f]);
+                        im = fma(Fi[f], Br[f], im);
+                        ar[f] = re;
+                        ai[f] = im;
                     }
                 }
             }
-        for (uint32_t comp = 0; comp < 2; comp++)
-            or_fft_inverse_add(N, (double*)(acc + comp * M), out + comp * N);
-        free(F);
-        free(acc);
+        for (uint32_t comp = 0; comp < 2; comp++) {
+            dit_inverse_soa(M, Ar[comp], Ai[comp], tab->W);
+            uint32_t* o = out + comp * N;
+            for (uint32_t j = 0; j < M; j++) {
+                const double wr = fma(Ar[comp][j], tab->UT[j].re, -(Ai[comp][j] * tab->UT[j].im));
+                const double wi = fma(Ar[comp][j], tab->UT[j].im, Ai[comp][j] * tab->UT[j].re);
+                o[j] += (uint32_t)(uint64_t)llrint(wr);
+                o[j + M] += (uint32_t)(uint64_t)llrint(wi);
+            }
+        }
     }
     free(dig);
     return 0;

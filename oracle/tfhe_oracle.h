@@ -92,6 +92,7 @@ typedef struct {
     uint32_t* bk;       /* torus form [n][(k+1)l][k+1][N] */
     uint32_t* ksk;      /* [N][t][base-1][n+1] */
     double* bk_fft;     /* [n][(k+1)l][k+1][N/2][2] (re,im), DIF bit-reversed order */
+    double* bk_fft_soa; /* same values, [..][k+1][re[N/2], im[N/2]] (vectorisable MAC) */
 } or_keyset;
 
 /* Deterministic key set from one seed. */
