@@ -1,8 +1,11 @@
-# A/B: bench each variant library given as arguments (names of paper_2407_19871_b200/lib_<v>.so)
+# A/B: for each variant (paper_2407_19871_b200/lib_<v>.so; "base" = the default build) run the
+# bit-exact parity subset and a short bench; one summary line per variant in gpurun_out/ab.txt
 echo "" > gpurun_out/ab.txt
 for v in base "$@"; do
-  if [ "$v" = base ]; then lib=""; else lib=paper_2407_19871_b200/lib_$v.so; fi
-  LOCPIR_B200_LIB=$lib timeout 300 python bench.py --steps 3 --warmup 1 --no-cpu-baseline > gpurun_out/ab_$v.log 2>&1
+  if [ "$v" = base ]; then lib=""; else lib=$PWD/paper_2407_19871_b200/lib_$v.so; fi
+  LOCPIR_B200_LIB=$lib timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "bit_exact or mux" > gpurun_out/ab_${v}_tests.log 2>&1
+  echo "$v tests rc=$? $(tail -1 gpurun_out/ab_${v}_tests.log)" >> gpurun_out/ab.txt
+  LOCPIR_B200_LIB=$lib timeout 300 python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-locpir > gpurun_out/ab_$v.log 2>&1
   python - "$v" <<'PY' >> gpurun_out/ab.txt
 import json, sys
 v = sys.argv[1]
