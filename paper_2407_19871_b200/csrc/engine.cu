@@ -5,6 +5,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -14,6 +15,7 @@
 #include "../../include/locpir_b200.h"
 #include "circuits.hpp"
 #include "kernels.cuh"
+#include "br_warp.cuh"
 #include "program.hpp"
 
 using namespace lpb;
@@ -112,6 +114,10 @@ struct locpir_b200_ctx {
     bool timing = false;
     Timer timer;
     int num_sms = 148;
+    // blind-rotate kernel: 0 = 64-thread CTA per ciphertext (k_blind_rotate, default),
+    // 1 = warp per ciphertext (k_blind_rotate_w, TMEM accumulators).  Env
+    // LOCPIR_B200_BR=cta|warp at context creation; it fixes the BK frequency layout.
+    int br_warp = 0;
 };
 
 namespace {
@@ -207,7 +213,17 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
         return;
     timed_begin(c, 0);
     const uint32_t mu = 0x20000000u;
-    if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+    if (c->br_warp) {
+        const uint32_t blocks = (count + W_CT - 1) / W_CT;
+        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+            k_blind_rotate_w<3, 7><<<blocks, 32 * W_CT, W_SMEM, c->stream>>>(
+                c->dp, items, count, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+            k_blind_rotate_w<2, 10><<<blocks, 32 * W_CT, W_SMEM, c->stream>>>(
+                c->dp, items, count, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else
+            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    } else if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
         k_blind_rotate<3, 7><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
                                                           c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
     else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
@@ -399,6 +415,12 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
         CK(cudaMemcpy(c->UT.p, UT.data(), UT.size() * sizeof(double2), cudaMemcpyHostToDevice));
         CK(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(KS_CT * p->N * sizeof(uint16_t))));
+        CK(cudaFuncSetAttribute(k_blind_rotate_w<3, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)W_SMEM));
+        CK(cudaFuncSetAttribute(k_blind_rotate_w<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)W_SMEM));
+        if (const char* br = getenv("LOCPIR_B200_BR"))
+            c->br_warp = strcmp(br, "warp") == 0;
     });
     if (rc != LOCPIR_B200_OK) {
         fprintf(stderr, "locpir_b200_ctx_create: %s\n", c->err.c_str());
@@ -447,7 +469,11 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
             dbk = tmp.p;
         }
         c->bkf.reserve(polys * FFT_M, c->stream, false);
-        k_bk_to_freq<<<(uint32_t)polys, 64, 0, c->stream>>>(dbk, c->bkf.p, c->W.p, c->TW.p);
+        if (c->br_warp)
+            k_bk_to_freq_w<<<(uint32_t)((polys + W_CT - 1) / W_CT), 32 * W_CT, 0, c->stream>>>(
+                dbk, c->bkf.p, c->W.p, c->TW.p, (uint32_t)polys);
+        else
+            k_bk_to_freq<<<(uint32_t)polys, 64, 0, c->stream>>>(dbk, c->bkf.p, c->W.p, c->TW.p);
         CK(cudaGetLastError());
         // KSK rows padded to n_stride words (zero padding)
         const size_t rows_ks = (size_t)c->p.N * c->p.ks_t * ((1u << c->p.ks_basebit) - 1);
