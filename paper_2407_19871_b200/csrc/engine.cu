@@ -118,6 +118,9 @@ struct locpir_b200_ctx {
     // 1 = warp per ciphertext (k_blind_rotate_w, TMEM accumulators).  Env
     // LOCPIR_B200_BR=cta|warp at context creation; it fixes the BK frequency layout.
     int br_warp = 0;
+    // small levels (fewer bootstraps than SMs) take the latency kernels
+    int small_levels = 1;
+    DevBuf<uint32_t> ks_partial;
 };
 
 namespace {
@@ -213,7 +216,16 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
         return;
     timed_begin(c, 0);
     const uint32_t mu = 0x20000000u;
-    if (c->br_warp) {
+    if (!c->br_warp && c->small_levels && count <= (uint32_t)c->num_sms) {
+        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+            k_blind_rotate_lat<3, 7><<<count, 128 * 3, sizeof(LatSmem<3>), c->stream>>>(
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+            k_blind_rotate_lat<2, 10><<<count, 128 * 2, sizeof(LatSmem<2>), c->stream>>>(
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else
+            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    } else if (c->br_warp) {
         const uint32_t blocks = (count + W_CT - 1) / W_CT;
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
             k_blind_rotate_w<3, 7><<<blocks, 32 * W_CT, W_SMEM, c->stream>>>(
@@ -241,6 +253,16 @@ void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
         return;
     timed_begin(c, 1);
     const uint32_t blocks = (count + KS_CT - 1) / KS_CT;
+    if (c->small_levels && blocks < (uint32_t)c->num_sms / 2) {
+        c->ks_partial.reserve((size_t)count * KS_SPLIT * c->dp.n_stride, c->stream, false);
+        k_keyswitch_split<<<dim3(count, KS_SPLIT), KS_THREADS, 0, c->stream>>>(
+            c->dp, items, c->pool_N.p, c->ksk.p, c->ks_partial.p);
+        k_ks_reduce<<<count, KS_THREADS, 0, c->stream>>>(c->dp, items, c->pool_N.p,
+                                                          c->ks_partial.p, c->pool_n.p);
+        CK(cudaGetLastError());
+        timed_end(c, 1);
+        return;
+    }
     const size_t smem = (size_t)KS_CT * c->p.N * sizeof(uint16_t);
     k_keyswitch<<<blocks, KS_THREADS, smem, c->stream>>>(c->dp, items, count, c->pool_N.p,
                                                          c->pool_n.p, c->ksk.p);
@@ -419,6 +441,12 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
                                 (int)W_SMEM));
         CK(cudaFuncSetAttribute(k_blind_rotate_w<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)W_SMEM));
+        CK(cudaFuncSetAttribute(k_blind_rotate_lat<3, 7>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<3>)));
+        CK(cudaFuncSetAttribute(k_blind_rotate_lat<2, 10>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<2>)));
+        if (const char* sl = getenv("LOCPIR_B200_SMALL"))
+            c->small_levels = strcmp(sl, "0") != 0;
         if (const char* br = getenv("LOCPIR_B200_BR"))
             c->br_warp = strcmp(br, "warp") == 0;
     });

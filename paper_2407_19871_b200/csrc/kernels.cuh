@@ -470,3 +470,197 @@ __global__ void k_fp64_peak(double* out, int iters)
 }
 
 }  // namespace lpb
+
+namespace lpb {
+
+// ---------------------------------------------------------------------------
+// Small-batch (latency) kernels, used when a circuit level has fewer bootstraps
+// than SMs (e.g. a single LocPIR query, BASELINE configs[0]).
+// ---------------------------------------------------------------------------
+
+// K2s: key switching split over KS_SPLIT coefficient ranges per ciphertext; the
+// partial sums (mod 2^32, order-free, so bit-exact) are reduced by k_ks_reduce.
+constexpr int KS_SPLIT = 32;
+
+__global__ void __launch_bounds__(KS_THREADS)
+    k_keyswitch_split(DevParams dp, const KsItem* __restrict__ items,
+                      const uint32_t* __restrict__ pool_N, const uint32_t* __restrict__ ksk,
+                      uint32_t* __restrict__ partial)
+{
+    const uint32_t g = blockIdx.x, split = blockIdx.y;
+    const KsItem it = items[g];
+    const uint32_t N = dp.N, per = N / KS_SPLIT;
+    const uint32_t prec = 1u << (32 - (1 + dp.basebit * dp.t));
+    const uint32_t col = threadIdx.x * KS_COLS;
+    if (col >= dp.n_stride)
+        return;
+    const uint32_t* a0 = pool_N + (size_t)it.in0 * dp.N_stride;
+    const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_N + (size_t)it.in1 * dp.N_stride : nullptr;
+    const size_t rs4 = dp.n_stride / 4;
+    const uint4* base = reinterpret_cast<const uint4*>(ksk + col);
+    uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+    for (uint32_t i = split * per; i < (split + 1) * per; i++) {
+        uint32_t v = __ldg(a0 + i);
+        if (a1)
+            v += __ldg(a1 + i);
+        const uint32_t w = (v + prec) >> 16;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t d = (w >> (14 - 2 * j)) & 3u;
+            if (d) {
+                const uint4 r = __ldg(base + ((size_t)i * 24 + j * 3 + (d - 1)) * rs4);
+                acc.x -= r.x;
+                acc.y -= r.y;
+                acc.z -= r.z;
+                acc.w -= r.w;
+            }
+        }
+    }
+    *reinterpret_cast<uint4*>(partial + ((size_t)g * KS_SPLIT + split) * dp.n_stride + col) = acc;
+}
+
+__global__ void __launch_bounds__(KS_THREADS)
+    k_ks_reduce(DevParams dp, const KsItem* __restrict__ items,
+                const uint32_t* __restrict__ pool_N, const uint32_t* __restrict__ partial,
+                uint32_t* __restrict__ pool_n)
+{
+    const uint32_t g = blockIdx.x;
+    const KsItem it = items[g];
+    for (uint32_t col = threadIdx.x; col < dp.n_stride; col += blockDim.x) {
+        uint32_t v = 0;
+        if (col == dp.n) {
+            v = pool_N[(size_t)it.in0 * dp.N_stride + dp.N] + it.off;
+            if (it.in1 != SLOT_NONE)
+                v += pool_N[(size_t)it.in1 * dp.N_stride + dp.N];
+        }
+        for (int s = 0; s < KS_SPLIT; s++)
+            v += partial[((size_t)g * KS_SPLIT + s) * dp.n_stride + col];
+        pool_n[(size_t)it.out * dp.n_stride + col] = v;
+    }
+}
+
+// K1l: blind rotation with the 2l digit transforms of one ciphertext in parallel,
+// one 64-thread group each (named barrier per group); the frequency-domain MAC runs
+// in the oracle's row order (rows 0..2l-1, same fma chain), so results stay
+// bit-exact; groups 0 and 1 then run the two inverse transforms in parallel.
+template <int L>
+struct LatSmem {
+    uint32_t acc[2][1024];
+    double2 tws[FFT_M];
+    double2 F[2 * L][FFT_M];              // digit spectra, slot layout [q*64 + t]
+    double2 tiles[2 * L][2][XTILE];       // per group: cross-warp tile, intra-warp tile
+    uint16_t abar[MAX_N + 1];
+};
+
+__device__ __forceinline__ void group_bar(int id)
+{
+    asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
+}
+
+template <int L, int BGBIT>
+__global__ void __launch_bounds__(128 * L, 1)
+    k_blind_rotate_lat(DevParams dp, const BrItem* __restrict__ items,
+                       const uint32_t* __restrict__ pool_n, uint32_t* __restrict__ pool_N,
+                       const double2* __restrict__ bkf, const double2* __restrict__ W,
+                       const double2* __restrict__ TW, uint32_t mu)
+{
+    extern __shared__ __align__(16) uint8_t smem_l[];
+    LatSmem<L>& S = *reinterpret_cast<LatSmem<L>*>(smem_l);
+    const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
+    const BrItem it = items[blockIdx.x];
+    const uint32_t n = dp.n;
+    for (int j = threadIdx.x; j < FFT_M; j += blockDim.x)
+        S.tws[j] = TW[j];
+    {
+        const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
+        const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
+        for (uint32_t i = threadIdx.x; i <= n; i += blockDim.x) {
+            uint32_t v = (uint32_t)it.c0 * a0[i];
+            if (a1)
+                v += (uint32_t)it.c1 * a1[i];
+            if (i == n)
+                v += it.off;
+            S.abar[i] = (uint16_t)((v + (1u << 20)) >> 21);
+        }
+    }
+    __syncthreads();
+    {
+        const uint32_t e = (2048u - S.abar[n]) & 2047u;
+        for (int j = threadIdx.x; j < 1024; j += blockDim.x) {
+            S.acc[0][j] = 0;
+            const uint32_t idx = (uint32_t)(j - (int)e) & 2047u;
+            S.acc[1][j] = idx < 1024u ? mu : 0u - mu;
+        }
+    }
+    const Twiddles tw = load_twiddles(W, t);
+    const int bid = 1 + g;
+    auto bar = [bid] { group_bar(bid); };
+    auto wbar = [] { __syncwarp(); };
+    constexpr uint32_t HALF = 1u << (BGBIT - 1);
+    constexpr uint32_t MASK = (1u << BGBIT) - 1;
+    uint32_t OFF = 0;
+#pragma unroll
+    for (int q = 1; q <= L; q++)
+        OFF += HALF << (32 - q * BGBIT);
+    OFF += 1u << (31 - L * BGBIT);
+    constexpr int ROWS = 2 * L;
+    const int c = g / L, p = g % L;
+    const int sh = 32 - (p + 1) * BGBIT;
+
+    for (uint32_t i = 0; i < n; i++) {
+        __syncthreads();
+        const uint32_t a = S.abar[i];
+        if (a == 0)
+            continue;
+        // every group: digit (c, p) of (X^a - 1) ACC_c -> forward transform -> F[g]
+        {
+            double2 x[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int j = t + 64 * q;
+                const uint32_t lo = rot_read(S.acc[c], a, j) - S.acc[c][j] + OFF;
+                const uint32_t hi = rot_read(S.acc[c], a, j + 512) - S.acc[c][j + 512] + OFF;
+                const int dlo = (int)((lo >> sh) & MASK) - (int)HALF;
+                const int dhi = (int)((hi >> sh) & MASK) - (int)HALF;
+                x[q] = cmul(make_double2((double)dlo, (double)dhi), S.tws[j]);
+            }
+            fft_forward(x, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                S.F[g][q * 64 + t] = x[q];
+        }
+        __syncthreads();
+        // groups 0 / 1: MAC chain over the rows in oracle order, inverse, ACC update
+        if (g < 2) {
+            const int comp = g;
+            const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M + (size_t)comp * FFT_M;
+            double2 o[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                o[q] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int r = 0; r < ROWS; r++) {
+                const double2* row = bki + (size_t)r * 2 * FFT_M;
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    mac(o[q], S.F[r][q * 64 + t], ld_stream(row + q * 64 + t));
+            }
+            fft_inverse(o, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int j = t + 64 * q;
+                const double2 w = cmul(o[q], untwist(S.tws[j]));
+                S.acc[comp][j] += (uint32_t)__double2ll_rn(w.x);
+                S.acc[comp][j + 512] += (uint32_t)__double2ll_rn(w.y);
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t* out = pool_N + (size_t)it.out * dp.N_stride;
+    for (int j = threadIdx.x; j < 1024; j += blockDim.x)
+        out[j] = j == 0 ? S.acc[0][0] : 0u - S.acc[0][1024 - j];
+    if (threadIdx.x == 0)
+        out[1024] = S.acc[1][0];
+}
+
+}  // namespace lpb
