@@ -180,6 +180,16 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                 const uint32_t* out_slots, uint64_t scratch_first,
                                 int xor_tree, locpir_b200_gate_op* ops, uint64_t* count);
 
+/* ---- stage-wise parity hooks (diagnostics; host buffers, synchronous) -----------
+ * blind rotation + sample extraction of one combined LWE (n+1 words, the gate's
+ * linear form already applied) -> N-dim LWE (N+1 words): the pre-key-switch
+ * coefficients the parity ladder compares with the exact oracle. */
+int locpir_b200_debug_blind_rotate(locpir_b200_ctx* ctx, const uint32_t* lwe_n, uint64_t count,
+                                   uint32_t* out_N);
+/* key switch of N-dim LWEs (N+1 words each) -> n-dim (n+1 words each) */
+int locpir_b200_debug_keyswitch(locpir_b200_ctx* ctx, const uint32_t* lwe_N, uint64_t count,
+                                uint32_t* out_n);
+
 /* ---- instrumentation -------------------------------------------------------------
  * Per-kernel device time (CUDA events on the context stream) accumulated since the
  * last reset: [0] blind-rotate ms, [1] key-switch ms, [2] linear ms; launches in

@@ -74,6 +74,8 @@ SIGNATURES = [
     ("locpir_b200_loc_pir_program", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
       C.c_uint64, C.c_int, _ops, _u64p]),
+    ("locpir_b200_debug_blind_rotate", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
+    ("locpir_b200_debug_keyswitch", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_timing_enable", C.c_int, [_ctx, C.c_int]),
     ("locpir_b200_kernel_stats", C.c_int, [_ctx, C.POINTER(C.c_double), _u64p]),
     ("locpir_b200_fp64_peak", C.c_int, [_ctx, C.POINTER(C.c_double)]),

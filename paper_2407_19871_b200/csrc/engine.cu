@@ -697,6 +697,70 @@ int locpir_b200_gate_batch_host(locpir_b200_ctx* c, uint32_t kind, const uint32_
     });
 }
 
+int locpir_b200_debug_blind_rotate(locpir_b200_ctx* c, const uint32_t* lwe_n, uint64_t count,
+                                   uint32_t* out_N)
+{
+    return guarded(c, [&] {
+        if (count && (!lwe_n || !out_N))
+            throw std::invalid_argument("null buffer");
+        need_keys(c);
+        CK(cudaSetDevice(c->device));
+        if (c->pool_slots < count) {
+            int rc = locpir_b200_pool_reserve(c, count);
+            if (rc)
+                throw CudaError(c->err);
+        }
+        pool_copy(c, 0, count, lwe_n, nullptr, cudaMemcpyHostToDevice, true);
+        std::vector<BrItem> items(count);
+        for (uint64_t g = 0; g < count; g++)
+            items[g] = {(uint32_t)g, SLOT_NONE, 1, 0, 0u, (uint32_t)g};
+        if (count > c->scratch_slots) {
+            c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
+            c->scratch_slots = c->pool_N.n / c->dp.N_stride;
+        }
+        DevBuf<BrItem> d;
+        d.reserve(count + 1, c->stream, false);
+        CK(cudaMemcpyAsync(d.p, items.data(), count * sizeof(BrItem), cudaMemcpyHostToDevice,
+                           c->stream));
+        launch_br(c, d.p, (uint32_t)count);
+        CK(cudaMemcpy2DAsync(out_N, (size_t)(c->p.N + 1) * 4, c->pool_N.p, (size_t)c->dp.N_stride * 4,
+                             (size_t)(c->p.N + 1) * 4, count, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int locpir_b200_debug_keyswitch(locpir_b200_ctx* c, const uint32_t* lwe_N, uint64_t count,
+                                uint32_t* out_n)
+{
+    return guarded(c, [&] {
+        if (count && (!lwe_N || !out_n))
+            throw std::invalid_argument("null buffer");
+        need_keys(c);
+        CK(cudaSetDevice(c->device));
+        if (c->pool_slots < count) {
+            int rc = locpir_b200_pool_reserve(c, count);
+            if (rc)
+                throw CudaError(c->err);
+        }
+        if (count > c->scratch_slots) {
+            c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
+            c->scratch_slots = c->pool_N.n / c->dp.N_stride;
+        }
+        CK(cudaMemcpy2DAsync(c->pool_N.p, (size_t)c->dp.N_stride * 4, lwe_N, (size_t)(c->p.N + 1) * 4,
+                             (size_t)(c->p.N + 1) * 4, count, cudaMemcpyHostToDevice, c->stream));
+        std::vector<KsItem> items(count);
+        for (uint64_t g = 0; g < count; g++)
+            items[g] = {(uint32_t)g, SLOT_NONE, 0u, (uint32_t)g};
+        DevBuf<KsItem> d;
+        d.reserve(count + 1, c->stream, false);
+        CK(cudaMemcpyAsync(d.p, items.data(), count * sizeof(KsItem), cudaMemcpyHostToDevice,
+                           c->stream));
+        launch_ks(c, d.p, (uint32_t)count);
+        pool_copy(c, 0, count, nullptr, out_n, cudaMemcpyDeviceToHost, false);
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
 uint64_t locpir_b200_loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
 {
     return loc_pir_scratch(Q, R, l, m);

@@ -87,6 +87,9 @@ constexpr int MAX_N = 1023;
 #ifndef TWIST_REGS
 #define TWIST_REGS 0
 #endif
+#ifndef TWIST_TMEM
+#define TWIST_TMEM 0
+#endif
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 2
 #endif
@@ -185,13 +188,34 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     // exchange tiles: [0],[1] cross-warp (alternating), [2] intra-warp
     __shared__ __align__(16) double2 xbuf[3][XTILE];
     __shared__ uint16_t abar[MAX_N + 1];
-#if !TWIST_REGS
+#if !TWIST_REGS && !TWIST_TMEM
     __shared__ __align__(16) double2 tws[FFT_M];  // twist table psi^j
+#endif
+#if TWIST_TMEM
+    __shared__ uint32_t tmem_slot;
 #endif
 
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
-#if TWIST_REGS
+#if TWIST_TMEM
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t ttw = tmem_slot + ((uint32_t)(t & 32) << 16);
+    {
+        uint32_t v[32];
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            pack2(v + 4 * q, TW[t + 64 * q]);
+        tmem_st32(ttw, v);
+        tmem_wait_st();
+    }
+#elif TWIST_REGS
     double2 twr[8];  // this thread's twist factors psi^j, j = t + 64 q (untwist = conj / 512)
 #pragma unroll
     for (int q = 0; q < 8; q++)
@@ -279,12 +303,20 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 #endif
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
+#if TWIST_TMEM
+                uint32_t tv[32];
+                tmem_ld32(ttw, tv);
+#define TWIST(q) unpack2(tv + 4 * (q))
+#endif
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     const int dlo = (int)((tmp[q] >> sh) & MASK) - (int)HALF;
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
                     x[q] = cmul(make_double2((double)dlo, (double)dhi), TWIST(q));
                 }
+#if TWIST_TMEM
+#undef TWIST
+#endif
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
 #if BK_PREFETCH < 2
@@ -307,6 +339,11 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         // inverse transforms, round, accumulate into ACC
         fft_inverse(oA, tw, xbuf[xs], xbuf[2], t, bar, wbar);
         xs ^= 1;
+#if TWIST_TMEM
+        uint32_t tv[32];
+        tmem_ld32(ttw, tv);
+#define TWIST(q) unpack2(tv + 4 * (q))
+#endif
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
@@ -316,6 +353,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         }
         fft_inverse(oB, tw, xbuf[xs], xbuf[2], t, bar, wbar);
         xs ^= 1;
+#if TWIST_TMEM
+        tmem_ld32(ttw, tv);
+#endif
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
@@ -323,6 +363,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j] += (uint32_t)__double2ll_rn(w.x);
             acc[1][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
+#if TWIST_TMEM
+#undef TWIST
+#endif
     }
     __syncthreads();
     // ---- sample extraction at index 0 (N-dim LWE under the TRLWE key)
@@ -331,6 +374,13 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         o[j] = j == 0 ? acc[0][0] : 0u - acc[0][1024 - j];
     if (t == 0)
         o[1024] = acc[1][0];
+#if TWIST_TMEM
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (t < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem_slot));
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -264,6 +264,21 @@ class Context:
         self._c(lib().locpir_b200_loc_pir(self.h, Q, R, l, m, *[_u32(v) for v in arrs],
                                           scratch_first, int(bool(xor_tree))))
 
+    def debug_blind_rotate(self, lwe_n: np.ndarray) -> np.ndarray:
+        """Blind rotation + extraction of combined n-dim LWEs -> N-dim LWEs (pre-KS)."""
+        lwe_n = np.ascontiguousarray(lwe_n, np.uint32).reshape(-1, self.params.n + 1)
+        out = np.zeros((lwe_n.shape[0], self.params.N + 1), np.uint32)
+        self._c(lib().locpir_b200_debug_blind_rotate(self.h, lwe_n.ctypes.data, lwe_n.shape[0],
+                                                     out.ctypes.data))
+        return out
+
+    def debug_keyswitch(self, lwe_N: np.ndarray) -> np.ndarray:
+        lwe_N = np.ascontiguousarray(lwe_N, np.uint32).reshape(-1, self.params.N + 1)
+        out = np.zeros((lwe_N.shape[0], self.params.n + 1), np.uint32)
+        self._c(lib().locpir_b200_debug_keyswitch(self.h, lwe_N.ctypes.data, lwe_N.shape[0],
+                                                  out.ctypes.data))
+        return out
+
     def timing(self, on: bool):
         self._c(lib().locpir_b200_timing_enable(self.h, int(on)))
 

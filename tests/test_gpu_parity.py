@@ -290,3 +290,29 @@ def test_locpir_config_shapes_match_plaintext(dev, name, Q, R):
     assert np.array_equal(got, b.truth())
     assert ctx.counters()["bootstrap_units"] == b.units()
     prog.close()
+
+
+@pytest.mark.parametrize("level", [80, 128])
+@pytest.mark.parametrize("count", [3, 600])  # latency kernel (< SMs) and throughput kernel
+def test_pre_keyswitch_coefficients_equal_exact_oracle(dev, level, count, okeys80, okeys128,
+                                                       oracle):
+    """SURVEY §8(c) parity ladder: the N-dim extracted coefficients (before key switching)
+    equal the EXACT mod-2^32 schoolbook oracle -- stated FFT error bound 0."""
+    p, keys, ctx = dev[level]
+    ok = okeys80 if level == 80 else okeys128
+    rng = np.random.default_rng(level + count)
+    lwe = rng.integers(0, 2 ** 32, (count, p.n + 1), dtype=np.uint64).astype(np.uint32)
+    got = ctx.debug_blind_rotate(lwe)
+    for g in (0, count - 1):
+        assert np.array_equal(got[g], ok.blind_rotate_extract(lwe[g], mode=oracle.EXACT))
+
+
+@pytest.mark.parametrize("count", [5, 3000])  # split (small-level) and batched key switch
+def test_keyswitch_bit_exact_on_identical_inputs(dev, count, okeys128):
+    """K2 bit-exact against the oracle on identical N-dim inputs."""
+    p, keys, ctx = dev[128]
+    rng = np.random.default_rng(count)
+    lweN = rng.integers(0, 2 ** 32, (count, p.N + 1), dtype=np.uint64).astype(np.uint32)
+    got = ctx.debug_keyswitch(lweN)
+    for g in (0, count // 2, count - 1):
+        assert np.array_equal(got[g], okeys128.keyswitch(lweN[g]))
