@@ -120,6 +120,7 @@ struct locpir_b200_ctx {
     int br_warp = 0;
     // small levels (fewer bootstraps than SMs) take the latency kernels
     int small_levels = 1;
+    int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
     DevBuf<uint32_t> ks_partial;
 };
 
@@ -445,6 +446,8 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<3>)));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<2, 10>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<2>)));
+        if (const char* lp = getenv("LOCPIR_B200_L2PERSIST"))
+            c->l2_persist = strcmp(lp, "0") != 0;
         if (const char* sl = getenv("LOCPIR_B200_SMALL"))
             c->small_levels = strcmp(sl, "0") != 0;
         if (const char* br = getenv("LOCPIR_B200_BR"))
@@ -513,6 +516,26 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
                              c->stream));
         CK(cudaStreamSynchronize(c->stream));
         c->have_keys = true;
+        // Keep the frequency-domain BK resident in L2 (persisting access window): at cfg2
+        // scale the blind-rotate CTAs sweep all 62 MB of it out of step with each other.
+        if (c->l2_persist) {
+            int maxp = 0, maxw = 0;
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
+            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
+            const size_t bytes = c->bkf.n * sizeof(double2);
+            if (maxp > 0 && maxw > 0) {
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, maxp));
+                cudaStreamAttrValue v{};
+                v.accessPolicyWindow.base_ptr = c->bkf.p;
+                v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, maxw);
+                v.accessPolicyWindow.hitRatio =
+                    std::min(1.0f, (float)std::min<size_t>(bytes, maxp) / (float)v.accessPolicyWindow.num_bytes);
+                v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+                v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+                cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+                cudaGetLastError();
+            }
+        }
     });
 }
 

@@ -87,6 +87,9 @@ constexpr int MAX_N = 1023;
 #ifndef TWIST_REGS
 #define TWIST_REGS 0
 #endif
+#ifndef BK_EVICT_LAST
+#define BK_EVICT_LAST 1
+#endif
 #ifndef TWIST_TMEM
 #define TWIST_TMEM 0
 #endif
@@ -161,9 +164,18 @@ __device__ __forceinline__ double2 untwist(double2 tw)
 __device__ __forceinline__ double2 ld_stream(const double2* p)
 {
     double2 v;
+#if BK_EVICT_LAST
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(p));
+#else
     asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
                  : "=d"(v.x), "=d"(v.y)
                  : "l"(p));
+#endif
     return v;
 }
 
