@@ -42,6 +42,17 @@ def flop_per_br(n=630, k=1, l=3, N=1024):
     return n * (((k + 1) * l + (k + 1)) * F_FFT + (k + 1) ** 2 * l * (N // 2) * 8)
 
 
+def committed_traffic(kernel="k_blind_rotate<3, 7>"):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one full-size launch, from the
+    committed ncu capture (profiles/r01_traffic.json); None when absent."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
+        k = d["kernels"][kernel]
+        return k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
+    except Exception:
+        return None
+
+
 def workload_config(n_gpus):
     return {
         "workload": "cfg2: 65,536 independent bootstrapped NAND gates per GPU, 128-bit TFHE "
@@ -358,7 +369,12 @@ def run_b200(args):
             "roofline": {
                 "bound": "fp64", "kernel": "k_blind_rotate<3,7> (K1)",
                 "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved_tflops / peak if peak else None, "traffic": None,
+                "frac": achieved_tflops / peak if peak else None,
+                "traffic": committed_traffic() if G == GATES_PER_GPU else None,
+                "traffic_unit": "bytes per launch (DRAM read+write, ncu capture in "
+                                "profiles/r01_traffic.json)",
+                "algorithmic_bytes_per_launch": G * (2 * 4 * (params.n + 1) + 4 * (params.N + 1))
+                                                + params.bk_words() * 8,
                 "flop_per_unit": flop_per_br(), "units_per_launch": G,
                 "avg_launch_ms": avg_br_ms,
                 "peak_source": "measured live on this GPU: k_fp64_peak DFMA microbenchmark "
