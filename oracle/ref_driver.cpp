@@ -150,6 +150,40 @@ static int golden()
                 }
         put_words("locpir_synthetic_N_l_m_got_expected_units_xnor_mux_and_xor_not_pred", rows);
     }
+    // the 9-city KDCA table end to end (acceptance.cpp:180-237), clear engine: grid-encoded
+    // boxes (dataset.hpp:232-259), services, interior query points + one outside point,
+    // and the reference's own retrieved values
+    {
+        const FixedPointFormat fmt{9, 7};
+        auto [records, dataset] = load_dataset("/root/reference/proj/data/kdca_2021-10-26.csv", fmt);
+        GateEngine eng = GateEngine::make_clear();
+        std::vector<uint64_t> services;
+        std::vector<uint32_t> boxes, svc, queries, expected;
+        for (const RegionRecord& r : records) {
+            services.push_back(r.service);
+            for (double v : {r.lat1, r.lat2, r.lon1, r.lon2})
+                boxes.push_back((uint32_t)(int32_t)scale_to_grid(v, fmt));
+            svc.push_back((uint32_t)r.service);
+        }
+        auto regions = encode_regions(records, fmt, eng,
+                                      trivial_services(services, dataset.service_bits, eng));
+        std::vector<std::pair<double, double>> pts;
+        for (const RegionRecord& r : records)
+            pts.push_back({(r.lat1 + r.lat2) / 2, (r.lon1 + r.lon2) / 2});
+        pts.push_back({33.0, 127.0});
+        for (auto [lat, lon] : pts) {
+            const PlainWord px = encode_fixed(lat, fmt), py = encode_fixed(lon, fmt);
+            queries.push_back((uint32_t)(int32_t)px.signed_value());
+            queries.push_back((uint32_t)(int32_t)py.signed_value());
+            auto out = loc_pir(constant_word(px, eng), constant_word(py, eng), regions, eng, 1);
+            expected.push_back((uint32_t)decrypt_service(out, eng));
+        }
+        put_words("city_boxes_grid_x1_x2_y1_y2_int32", boxes);
+        put_words("city_services", svc);
+        put_words("city_service_bits", {dataset.service_bits});
+        put_words("city_queries_grid_xy_int32", queries);
+        put_words("city_expected", expected);
+    }
     // sizes (acceptance.cpp:38-101)
     {
         put_words("sample_bytes_sec80_sec128",

@@ -316,3 +316,58 @@ def test_keyswitch_bit_exact_on_identical_inputs(dev, count, okeys128):
     got = ctx.debug_keyswitch(lweN)
     for g in (0, count // 2, count - 1):
         assert np.array_equal(got[g], okeys128.keyswitch(lweN[g]))
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_city_table_end_to_end_matches_reference(dev, golden, level):
+    """acceptance.cpp:180-237: the 9-city KDCA table, interior point of every box returns
+    its service and an open-sea point returns 0 -- expected values produced by the
+    reference itself (tests/golden/ref_vectors.json, city_*), boundaries as trivial words
+    (dataset.hpp:250-253), services and queries encrypted."""
+    from paper_2407_19871_b200 import GateEngine
+    from paper_2407_19871_b200.circuits import (CipherWord, EncodedRegion, FixedPointFormat,
+                                                PlainWord, ServiceCiphertext, constant_word,
+                                                decrypt_service, encrypt_word, loc_pir)
+    p, keys, ctx = dev[level]
+    fmt = FixedPointFormat(9, 7)
+    m = golden["city_service_bits"][0]
+    boxes = np.array(golden["city_boxes_grid_x1_x2_y1_y2_int32"], np.uint32).view(np.int32)
+    boxes = boxes.reshape(-1, 4)
+    eng = GateEngine(ctx, keys, seed=31)
+    eng._next_slot = 0
+    regions = []
+    for i, (x1, x2, y1, y2) in enumerate(boxes):
+        w = [constant_word(PlainWord.from_integer(int(v), fmt), eng) for v in (x1, x2, y1, y2)]
+        svc = golden["city_services"][i]
+        bits = eng.encrypt_many([(svc >> j) & 1 for j in range(m)])
+        regions.append(EncodedRegion(*w, ServiceCiphertext(bits), i))
+    q = np.array(golden["city_queries_grid_xy_int32"], np.uint32).view(np.int32).reshape(-1, 2)
+    outs = []
+    with eng.batch():
+        for gx, gy in q:
+            x = encrypt_word(PlainWord.from_integer(int(gx), fmt), eng)
+            y = encrypt_word(PlainWord.from_integer(int(gy), fmt), eng)
+            outs.append(loc_pir(x, y, regions, eng, tree=True))
+    got = [decrypt_service(o, eng) for o in outs]
+    assert got == golden["city_expected"]
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_output_noise_over_1e5_gates(dev, level):
+    """acceptance.cpp:377-410: over 10^5 bootstrapped gates every output phase lies within
+    1/16 of its nominal +-1/8 (here the real bootstrap replaces the refresh stand-in)."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[level]
+    G = 100_000
+    rng = np.random.default_rng(level)
+    A = rng.integers(0, 2, G).astype(np.uint8)
+    B = rng.integers(0, 2, G).astype(np.uint8)
+    a = keys.encrypt_bits(A, 500 + level)
+    b = keys.encrypt_bits(B, 600 + level)
+    out = ctx.gate_batch_host(_abi.XOR, a, b)   # XOR doubles input noise: the hardest form
+    assert np.array_equal(keys.decrypt_bits(out), A ^ B)
+    n = p.n
+    ph = (out[:, n].astype(np.int64) - (out[:, :n].astype(np.int64) @ keys.lwe_key.astype(np.int64)))
+    ph = (((ph + 2 ** 31) % 2 ** 32) - 2 ** 31) / 2 ** 32
+    err = np.abs(ph - np.where(A ^ B, 0.125, -0.125))
+    assert err.max() < 1 / 16
