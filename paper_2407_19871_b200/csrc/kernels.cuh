@@ -403,11 +403,17 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 // warp (all lanes work on the same ciphertext), so the row choice is a
 // warp-uniform branch and each selected row costs one add per column.
 // ---------------------------------------------------------------------------
-constexpr int KS_CT = 16;
+#ifndef KS_MINB
+#define KS_MINB 4
+#endif
+#ifndef KS_CT_DEF
+#define KS_CT_DEF 16
+#endif
+constexpr int KS_CT = KS_CT_DEF;
 constexpr int KS_COLS = 4;
 constexpr int KS_THREADS = 160;  // 640 columns >= n_stride
 
-__global__ void __launch_bounds__(KS_THREADS, 2)
+__global__ void __launch_bounds__(KS_THREADS, KS_MINB)
     k_keyswitch(DevParams dp, const KsItem* __restrict__ items, uint32_t count,
                 const uint32_t* __restrict__ pool_N, uint32_t* __restrict__ pool_n,
                 const uint32_t* __restrict__ ksk)
