@@ -16,6 +16,7 @@
 #include "circuits.hpp"
 #include "kernels.cuh"
 #include "br_warp.cuh"
+#include "br_pair.cuh"
 #include "program.hpp"
 
 using namespace lpb;
@@ -118,6 +119,7 @@ struct locpir_b200_ctx {
     // 1 = warp per ciphertext (k_blind_rotate_w, TMEM accumulators).  Env
     // LOCPIR_B200_BR=cta|warp at context creation; it fixes the BK frequency layout.
     int br_warp = 0;
+    int br_pair = 0;  // LOCPIR_B200_BR=pair: paired digit transforms (k_blind_rotate_pair)
     // small levels (fewer bootstraps than SMs) take the latency kernels
     int small_levels = 1;
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
@@ -223,6 +225,15 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
                 c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
             k_blind_rotate_lat<2, 10><<<count, 128 * 2, sizeof(LatSmem<2>), c->stream>>>(
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else
+            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    } else if (c->br_pair) {
+        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+            k_blind_rotate_pair<3, 7><<<count, 64, sizeof(PairSmem), c->stream>>>(
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+            k_blind_rotate_pair<2, 10><<<count, 64, sizeof(PairSmem), c->stream>>>(
                 c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
@@ -450,8 +461,14 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             c->l2_persist = strcmp(lp, "0") != 0;
         if (const char* sl = getenv("LOCPIR_B200_SMALL"))
             c->small_levels = strcmp(sl, "0") != 0;
-        if (const char* br = getenv("LOCPIR_B200_BR"))
+        CK(cudaFuncSetAttribute(k_blind_rotate_pair<3, 7>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem)));
+        CK(cudaFuncSetAttribute(k_blind_rotate_pair<2, 10>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem)));
+        if (const char* br = getenv("LOCPIR_B200_BR")) {
             c->br_warp = strcmp(br, "warp") == 0;
+            c->br_pair = strcmp(br, "pair") == 0;
+        }
     });
     if (rc != LOCPIR_B200_OK) {
         fprintf(stderr, "locpir_b200_ctx_create: %s\n", c->err.c_str());

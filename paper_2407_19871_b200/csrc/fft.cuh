@@ -269,4 +269,198 @@ __device__ __forceinline__ void fft_inverse(double2 x[8], const Twiddles& tw, do
     dit(x[3], x[7], conj2(mul_i(tw.p0b)));
 }
 
+// ---- paired transforms: two independent polynomials per thread in lockstep; they share
+// every exchange barrier and the compiler interleaves their butterflies (2x ILP).  The
+// per-polynomial arithmetic is exactly fft_forward / fft_inverse.
+__device__ __forceinline__ void pass0_fwd(double2 x[8], const Twiddles& tw)
+{
+    dif(x[0], x[4], tw.p0a);
+    dif(x[1], x[5], tw.p0b);
+    dif(x[2], x[6], mul_i(tw.p0a));
+    dif(x[3], x[7], mul_i(tw.p0b));
+    dif(x[0], x[2], tw.p0c);
+    dif(x[1], x[3], mul_i(tw.p0c));
+    dif(x[4], x[6], tw.p0c);
+    dif(x[5], x[7], mul_i(tw.p0c));
+    dif(x[0], x[1], tw.p0d);
+    dif(x[2], x[3], tw.p0d);
+    dif(x[4], x[5], tw.p0d);
+    dif(x[6], x[7], tw.p0d);
+}
+__device__ __forceinline__ void pass1_fwd(double2 x[8], const Twiddles& tw)
+{
+    dif(x[0], x[4], tw.p1a);
+    dif(x[1], x[5], tw.p1b);
+    dif(x[2], x[6], mul_i(tw.p1a));
+    dif(x[3], x[7], mul_i(tw.p1b));
+    dif(x[0], x[2], tw.p1c);
+    dif(x[1], x[3], mul_i(tw.p1c));
+    dif(x[4], x[6], tw.p1c);
+    dif(x[5], x[7], mul_i(tw.p1c));
+    dif(x[0], x[1], tw.p1d);
+    dif(x[2], x[3], tw.p1d);
+    dif(x[4], x[5], tw.p1d);
+    dif(x[6], x[7], tw.p1d);
+}
+__device__ __forceinline__ void pass2_fwd(double2 x[8], const Twiddles& tw)
+{
+    dif_1(x[0], x[4]);
+    dif(x[1], x[5], tw.w64);
+    dif_i(x[2], x[6]);
+    dif(x[3], x[7], mul_i(tw.w64));
+    dif_1(x[0], x[2]);
+    dif_i(x[1], x[3]);
+    dif_1(x[4], x[6]);
+    dif_i(x[5], x[7]);
+    dif_1(x[0], x[1]);
+    dif_1(x[2], x[3]);
+    dif_1(x[4], x[5]);
+    dif_1(x[6], x[7]);
+}
+__device__ __forceinline__ void pass2_inv(double2 x[8], const Twiddles& tw)
+{
+    dit_1(x[0], x[1]);
+    dit_1(x[2], x[3]);
+    dit_1(x[4], x[5]);
+    dit_1(x[6], x[7]);
+    dit_1(x[0], x[2]);
+    dit_mi(x[1], x[3]);
+    dit_1(x[4], x[6]);
+    dit_mi(x[5], x[7]);
+    dit_1(x[0], x[4]);
+    dit(x[1], x[5], conj2(tw.w64));
+    dit_mi(x[2], x[6]);
+    dit(x[3], x[7], conj2(mul_i(tw.w64)));
+}
+__device__ __forceinline__ void pass1_inv(double2 x[8], const Twiddles& tw)
+{
+    dit(x[0], x[1], conj2(tw.p1d));
+    dit(x[2], x[3], conj2(tw.p1d));
+    dit(x[4], x[5], conj2(tw.p1d));
+    dit(x[6], x[7], conj2(tw.p1d));
+    dit(x[0], x[2], conj2(tw.p1c));
+    dit(x[1], x[3], conj2(mul_i(tw.p1c)));
+    dit(x[4], x[6], conj2(tw.p1c));
+    dit(x[5], x[7], conj2(mul_i(tw.p1c)));
+    dit(x[0], x[4], conj2(tw.p1a));
+    dit(x[1], x[5], conj2(tw.p1b));
+    dit(x[2], x[6], conj2(mul_i(tw.p1a)));
+    dit(x[3], x[7], conj2(mul_i(tw.p1b)));
+}
+__device__ __forceinline__ void pass0_inv(double2 x[8], const Twiddles& tw)
+{
+    dit(x[0], x[1], conj2(tw.p0d));
+    dit(x[2], x[3], conj2(tw.p0d));
+    dit(x[4], x[5], conj2(tw.p0d));
+    dit(x[6], x[7], conj2(tw.p0d));
+    dit(x[0], x[2], conj2(tw.p0c));
+    dit(x[1], x[3], conj2(mul_i(tw.p0c)));
+    dit(x[4], x[6], conj2(tw.p0c));
+    dit(x[5], x[7], conj2(mul_i(tw.p0c)));
+    dit(x[0], x[4], conj2(tw.p0a));
+    dit(x[1], x[5], conj2(tw.p0b));
+    dit(x[2], x[6], conj2(mul_i(tw.p0a)));
+    dit(x[3], x[7], conj2(mul_i(tw.p0b)));
+}
+
+// cross tiles c0/c1 are single-buffered: the leading barrier orders this write after
+// every thread's previous read of the same tile.
+template <class Bar, class WBar>
+__device__ __forceinline__ void fft_forward2(double2 x0[8], double2 x1[8], const Twiddles& tw,
+                                             double2* c0, double2* c1, double2* w0, double2* w1,
+                                             int t, Bar bar, WBar wbar)
+{
+    pass0_fwd(x0, tw);
+    pass0_fwd(x1, tw);
+    bar();
+    {
+        double2* a = c0 + slot_of(0, t >> 3, t & 7);
+        double2* b = c1 + slot_of(0, t >> 3, t & 7);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            a[72 * q] = x0[q];
+            b[72 * q] = x1[q];
+        }
+        bar();
+        const double2* ra = c0 + slot_of(t >> 3, 0, t & 7);
+        const double2* rb = c1 + slot_of(t >> 3, 0, t & 7);
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            x0[m] = ra[9 * m];
+            x1[m] = rb[9 * m];
+        }
+    }
+    pass1_fwd(x0, tw);
+    pass1_fwd(x1, tw);
+    {
+        wbar();
+        double2* a = w0 + slot_of(t >> 3, 0, t & 7);
+        double2* b = w1 + slot_of(t >> 3, 0, t & 7);
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            a[9 * m] = x0[m];
+            b[9 * m] = x1[m];
+        }
+        wbar();
+        const double2* ra = w0 + slot_of(t >> 3, t & 7, 0);
+        const double2* rb = w1 + slot_of(t >> 3, t & 7, 0);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            x0[q] = ra[q];
+            x1[q] = rb[q];
+        }
+    }
+    pass2_fwd(x0, tw);
+    pass2_fwd(x1, tw);
+}
+
+template <class Bar, class WBar>
+__device__ __forceinline__ void fft_inverse2(double2 x0[8], double2 x1[8], const Twiddles& tw,
+                                             double2* c0, double2* c1, double2* w0, double2* w1,
+                                             int t, Bar bar, WBar wbar)
+{
+    pass2_inv(x0, tw);
+    pass2_inv(x1, tw);
+    {
+        wbar();
+        double2* a = w0 + slot_of(t >> 3, t & 7, 0);
+        double2* b = w1 + slot_of(t >> 3, t & 7, 0);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            a[q] = x0[q];
+            b[q] = x1[q];
+        }
+        wbar();
+        const double2* ra = w0 + slot_of(t >> 3, 0, t & 7);
+        const double2* rb = w1 + slot_of(t >> 3, 0, t & 7);
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            x0[m] = ra[9 * m];
+            x1[m] = rb[9 * m];
+        }
+    }
+    pass1_inv(x0, tw);
+    pass1_inv(x1, tw);
+    bar();
+    {
+        double2* a = c0 + slot_of(t >> 3, 0, t & 7);
+        double2* b = c1 + slot_of(t >> 3, 0, t & 7);
+#pragma unroll
+        for (int m = 0; m < 8; m++) {
+            a[9 * m] = x0[m];
+            b[9 * m] = x1[m];
+        }
+        bar();
+        const double2* ra = c0 + slot_of(0, t >> 3, t & 7);
+        const double2* rb = c1 + slot_of(0, t >> 3, t & 7);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            x0[q] = ra[72 * q];
+            x1[q] = rb[72 * q];
+        }
+    }
+    pass0_inv(x0, tw);
+    pass0_inv(x1, tw);
+}
+
 }  // namespace lpb
