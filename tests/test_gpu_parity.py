@@ -371,3 +371,80 @@ def test_output_noise_over_1e5_gates(dev, level):
     ph = (((ph + 2 ** 31) % 2 ** 32) - 2 ** 31) / 2 ** 32
     err = np.abs(ph - np.where(A ^ B, 0.125, -0.125))
     assert err.max() < 1 / 16
+
+
+def _random_program(rng, n_inputs, n_ops, first_slot):
+    """Random SSA gate DAG over n_inputs input slots; returns (ops, plaintext evaluator)."""
+    from paper_2407_19871_b200 import _abi
+    kinds = [_abi.AND, _abi.OR, _abi.XOR, _abi.XNOR, _abi.NAND, _abi.NOR, _abi.MUX, _abi.NOT,
+             _abi.COPY, _abi.CONST]
+    live = list(range(n_inputs))
+    ops = []
+    nxt = first_slot
+    for _ in range(n_ops):
+        k = kinds[rng.integers(len(kinds))]
+        a, b, c = (int(live[rng.integers(len(live))]) for _ in range(3))
+        if k == _abi.CONST:
+            a = int(rng.integers(2))
+        ops.append((int(k), a, b, c, nxt))
+        live.append(nxt)
+        nxt += 1
+    return ops
+
+
+def _eval_plain(ops, vals):
+    from paper_2407_19871_b200 import _abi
+    v = dict(vals)
+    f = {_abi.AND: lambda a, b: a & b, _abi.OR: lambda a, b: a | b, _abi.XOR: lambda a, b: a ^ b,
+         _abi.XNOR: lambda a, b: 1 - (a ^ b), _abi.NAND: lambda a, b: 1 - (a & b),
+         _abi.NOR: lambda a, b: 1 - (a | b)}
+    for k, a, b, c, o in ops:
+        if k in f:
+            v[o] = f[k](v[a], v[b])
+        elif k == _abi.MUX:
+            v[o] = v[b] if v[a] else v[c]
+        elif k == _abi.NOT:
+            v[o] = 1 - v[a]
+        elif k == _abi.COPY:
+            v[o] = v[a]
+        else:
+            v[o] = a
+    return v
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_random_gate_programs_level_scheduled(dev, seed):
+    """The circuit scheduler (csrc/program.hpp) on random DAGs of every gate kind: decrypted
+    outputs equal plaintext evaluation; the plan's bootstrap count equals the reference
+    accounting (MUX = 2 units, free gates 0)."""
+    from paper_2407_19871_b200 import _abi, plan
+    p, keys, ctx = dev[80]
+    rng = np.random.default_rng(seed)
+    n_in, n_ops = 48, 400
+    ops = _random_program(rng, n_in, n_ops, n_in)
+    bits = rng.integers(0, 2, n_in).astype(np.uint8)
+    ctx.pool_reserve(n_in + n_ops)
+    ctx.h2d(0, keys.encrypt_bits(bits, 900 + seed))
+    ctx.counters_reset()
+    ctx.run(ops)
+    want = _eval_plain(ops, {i: int(bits[i]) for i in range(n_in)})
+    got = keys.decrypt_bits(ctx.d2h(n_in, n_ops))
+    assert [int(x) for x in got] == [want[n_in + i] for i in range(n_ops)]
+    units = sum(2 if k == _abi.MUX else (0 if k in (_abi.NOT, _abi.COPY, _abi.CONST) else 1)
+                for k, *_ in ops)
+    assert ctx.counters()["bootstrap_units"] == units
+    assert plan(ops)["blind_rotations"] == units
+
+
+def test_loc_pir_c_abi_entry(dev):
+    """locpir_b200_loc_pir (the batched circuits.hpp:276-324 entry point) directly."""
+    from paper_2407_19871_b200 import workloads as W
+    p, keys, ctx = dev[128]
+    b = W.make_batch(3, 5, 16, 4, seed=77)
+    b.x[1] = (b.boxes[2, 0] + b.boxes[2, 1]) // 2
+    b.y[1] = (b.boxes[2, 2] + b.boxes[2, 3]) // 2
+    lay = W.PoolLayout(b)
+    ctx.pool_reserve(lay.total)
+    W.load_batch(ctx, keys, b, lay, seed=78)
+    ctx.loc_pir(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.bnd, lay.svc, lay.out, lay.scratch)
+    assert np.array_equal(W.read_results(ctx, keys, b, lay), b.truth())
