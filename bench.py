@@ -216,6 +216,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
     plaintext XOR of the payloads of all containing boxes."""
     import torch
     from paper_2407_19871_b200 import ClientKeys, Context, TfheParams, workloads as W
+    from paper_2407_19871_b200.engine import plan
     out = {}
     ctx80 = keys80 = None
     for name, (sec, Qfull, R, l, m, enc) in W.CONFIGS.items():
@@ -233,30 +234,37 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
         lay = W.PoolLayout(b)
         ctx.pool_reserve(lay.total)
         W.load_batch(ctx, keys, b, lay, seed=5000 + rank)
-        prog = W.program(ctx, b, lay)
-        prog.launch()  # warm-up
-        torch.cuda.synchronize()
-        reps = 3 if b.units() < 200000 else 1
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            prog.launch()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = max_over_ranks(e0.elapsed_time(e1) / reps)
-        ok = bool(np.array_equal(W.read_results(ctx, keys, b, lay), b.truth()))
-        out[name] = {
-            "queries_per_s": ws * Q / (ms / 1e3), "ms_per_batch": ms, "queries_per_gpu": Q,
-            "full_batch_queries": Qfull, "boxes": R, "l": l, "m": m, "security_bits": sec,
-            "encrypted_boundaries": enc, "bootstrap_units_per_query": b.units() // Q,
-            "levels_launched": prog.kernels, "units_per_s": ws * b.units() / (ms / 1e3),
-            "correct": ok,
-            "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
-                                                       "(per-query cost is batch-independent "
-                                                       "once the GPU is saturated)",
-        }
-        prog.close()
+        # folded: flagged plaintext-boundary mode, not the reference count
+        for folded in ((False, True) if not enc else (False,)):
+            ops = W.program_ops(b, lay, True, folded)
+            units = plan(ops)["blind_rotations"]
+            prog = ctx.program(ops)
+            prog.launch()  # warm-up
+            torch.cuda.synchronize()
+            reps = 3 if units < 200000 else 1
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                prog.launch()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = max_over_ranks(e0.elapsed_time(e1) / reps)
+            ok = bool(np.array_equal(W.read_results(ctx, keys, b, lay), b.truth()))
+            out[name + ("_folded" if folded else "")] = {
+                "queries_per_s": ws * Q / (ms / 1e3), "ms_per_batch": ms, "queries_per_gpu": Q,
+                "full_batch_queries": Qfull, "boxes": R, "l": l, "m": m, "security_bits": sec,
+                "encrypted_boundaries": enc, "bootstrap_units_per_query": units // Q,
+                "reference_units_per_query": b.units() // Q,
+                "levels_launched": prog.kernels, "units_per_s": ws * units / (ms / 1e3),
+                "correct": ok,
+                "mode": ("flagged: plaintext boundaries constant-folded (not the reference "
+                         "gate count)") if folded else "reference circuit (N(12l+2m+3) units)",
+                "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
+                                                           "(per-query cost is batch-independent "
+                                                           "once the GPU is saturated)",
+            }
+            prog.close()
     if ctx80 is not None:
         ctx80.close()
     return out

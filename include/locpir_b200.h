@@ -48,6 +48,8 @@ extern "C" {
 #define LOCPIR_B200_NOR 7
 #define LOCPIR_B200_COPY 8 /* free: out = in0 */
 #define LOCPIR_B200_CONST 9 /* free: out = trivial sample encode_bit(in0 != 0) (gate_engine.hpp:174-179) */
+#define LOCPIR_B200_ANDNY 10 /* AND(NOT in0, in1): one bootstrap, form (-1/8, -1, +1) */
+#define LOCPIR_B200_ORNY 11  /* OR(NOT in0, in1):  one bootstrap, form (+1/8, -1, +1) */
 
 /* Full TFHE parameter set (extends TlweParams {n, sigma}, torus.hpp:71-110). */
 typedef struct locpir_b200_params {
@@ -189,6 +191,20 @@ int locpir_b200_debug_blind_rotate(locpir_b200_ctx* ctx, const uint32_t* lwe_n, 
 /* key switch of N-dim LWEs (N+1 words each) -> n-dim (n+1 words each) */
 int locpir_b200_debug_keyswitch(locpir_b200_ctx* ctx, const uint32_t* lwe_N, uint64_t count,
                                 uint32_t* out_n);
+
+/* ---- flagged mode: plaintext-boundary constant folding -------------
+ * The server's box boundaries are plaintext (dataset.hpp:250-253).  Comparing an
+ * encrypted word against a known word folds every XNOR into a free (or no) negation and
+ * every MUX into one AND/OR-with-negated-input bootstrap, and the first bit into a free
+ * gate: about 4l + 2m per region instead of 12l + 2m + 3 (the reference count model no
+ * longer applies -- hence a separate entry point).  boxes: [R][4] signed grid values
+ * (x1, x2, y1, y2) of l-bit two's-complement words; results decrypt identically. */
+uint64_t locpir_b200_loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m);
+int locpir_b200_loc_pir_folded_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                       const uint32_t* x_slots, const uint32_t* y_slots,
+                                       const int64_t* boxes, const uint32_t* svc_slots,
+                                       const uint32_t* out_slots, uint64_t scratch_first,
+                                       int xor_tree, locpir_b200_gate_op* ops, uint64_t* count);
 
 /* ---- instrumentation -------------------------------------------------------------
  * Per-kernel device time (CUDA events on the context stream) accumulated since the

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LOCPIR_B200_LIB") or os.path.join(HERE, "liblocpir_b200.so")
 
 OK, EINVAL, ELOGIC, ECUDA, ENOMEM = 0, -1, -2, -3, -4
-AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST = range(10)
+AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST, ANDNY, ORNY = range(12)
 SLOT_NONE = 0xFFFFFFFF
 
 
@@ -74,6 +74,10 @@ SIGNATURES = [
     ("locpir_b200_loc_pir_program", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
       C.c_uint64, C.c_int, _ops, _u64p]),
+    ("locpir_b200_loc_pir_folded_scratch", C.c_uint64, [C.c_uint32] * 4),
+    ("locpir_b200_loc_pir_folded_program", C.c_int,
+     [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.POINTER(C.c_int64), _u32p,
+      _u32p, C.c_uint64, C.c_int, _ops, _u64p]),
     ("locpir_b200_debug_blind_rotate", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_debug_keyswitch", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_timing_enable", C.c_int, [_ctx, C.c_int]),

@@ -112,4 +112,98 @@ inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint
     }
 }
 
+// ---- flagged mode: comparators against a PLAINTEXT word -------------
+// Same function as emit_less(a, B) for a known l-bit word B: with the sign bits flipped,
+// scan LSB -> MSB keeping t0 = [a' < B'] on the bits seen so far; at bit i
+//   b_i = 1 : t0 <- a_i ? t0 : 1 = OR(NOT a_i, t0)
+//   b_i = 0 : t0 <- a_i ? 0 : t0 = AND(NOT a_i, t0)
+// (XNOR(a_i, b_i) is a free negation or nothing).  While t0 is a known constant the
+// update is a free NOT / constant; otherwise one bootstrap (ANDNY / ORNY form).
+// Returns the slot of a < B (signed).
+struct MaybeConst {
+    bool is_const;
+    int value;
+    uint32_t slot;
+};
+
+inline uint32_t emit_less_plain(Emitter& e, const uint32_t* a, int64_t B, uint32_t l)
+{
+    const uint64_t u = (uint64_t)B;
+    MaybeConst t0{true, 0, 0};
+    for (uint32_t i = 0; i < l; i++) {
+        uint32_t bi = (uint32_t)((u >> i) & 1);
+        const bool sign = i + 1 == l;
+        if (sign)
+            bi ^= 1u;  // b' = NOT b at the sign position; a' = NOT a
+        if (t0.is_const) {
+            if ((bi == 1 && t0.value == 1) || (bi == 0 && t0.value == 0))
+                continue;  // t0 unchanged constant
+            // t0 <- NOT a'_i  (a'_i = a_i, or NOT a_{l-1} at the sign bit)
+            t0 = {false, 0, sign ? e.gate(LOCPIR_B200_COPY, a[i]) : e.gate(LOCPIR_B200_NOT, a[i])};
+            continue;
+        }
+        if (!sign)
+            t0.slot = e.gate(bi ? LOCPIR_B200_ORNY : LOCPIR_B200_ANDNY, a[i], t0.slot);
+        else  // NOT a'_{l-1} = a_{l-1}
+            t0.slot = e.gate(bi ? LOCPIR_B200_OR : LOCPIR_B200_AND, a[i], t0.slot);
+    }
+    if (t0.is_const)
+        return e.gate(LOCPIR_B200_CONST, (uint32_t)t0.value);
+    return t0.slot;
+}
+
+inline uint64_t loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
+{
+    const uint64_t per_region = 4ull * (l + 2) + 2 + 3 + m;
+    return (uint64_t)Q * ((uint64_t)R * per_region + (uint64_t)m * (1 + R));
+}
+
+// loc_pir with plaintext boxes [R][4] = (x1, x2, y1, y2): x1 <= x = NOT(x < x1).
+inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
+                                uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
+                                const int64_t* boxes, const uint32_t* svc, const uint32_t* out,
+                                uint64_t scratch_first, int xor_tree)
+{
+    Emitter e{&ops, scratch_first};
+    std::vector<uint32_t> masked((size_t)R * m);
+    for (uint32_t q = 0; q < Q; q++) {
+        const uint32_t* x = xs + (size_t)q * l;
+        const uint32_t* y = ys + (size_t)q * l;
+        for (uint32_t r = 0; r < R; r++) {
+            const int64_t* bx = boxes + (size_t)r * 4;
+            const uint32_t x_l = e.gate(LOCPIR_B200_NOT, emit_less_plain(e, x, bx[0], l));
+            const uint32_t x_r = emit_less_plain(e, x, bx[1], l);
+            const uint32_t y_l = e.gate(LOCPIR_B200_NOT, emit_less_plain(e, y, bx[2], l));
+            const uint32_t y_r = emit_less_plain(e, y, bx[3], l);
+            const uint32_t v1 = e.gate(LOCPIR_B200_AND, x_l, x_r);
+            const uint32_t v2 = e.gate(LOCPIR_B200_AND, y_l, y_r);
+            const uint32_t f = e.gate(LOCPIR_B200_AND, v1, v2);
+            for (uint32_t j = 0; j < m; j++)
+                masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc[(size_t)r * m + j]);
+        }
+        for (uint32_t j = 0; j < m; j++) {
+            const uint32_t dst = out[(size_t)q * m + j];
+            const uint32_t zero = e.gate(LOCPIR_B200_CONST, 0);
+            std::vector<uint32_t> lvl(R);
+            for (uint32_t r = 0; r < R; r++)
+                lvl[r] = masked[(size_t)r * m + j];
+            if (!xor_tree) {
+                uint32_t acc = zero;
+                for (uint32_t r = 0; r < R; r++)
+                    acc = e.gate(LOCPIR_B200_XOR, acc, lvl[r], 0xFFFFFFFFu, r + 1 == R ? dst : 0xFFFFFFFFu);
+                continue;
+            }
+            while (lvl.size() > 1) {
+                std::vector<uint32_t> nxt;
+                for (size_t i = 0; i + 1 < lvl.size(); i += 2)
+                    nxt.push_back(e.gate(LOCPIR_B200_XOR, lvl[i], lvl[i + 1]));
+                if (lvl.size() & 1)
+                    nxt.push_back(lvl.back());
+                lvl.swap(nxt);
+            }
+            e.gate(LOCPIR_B200_XOR, zero, lvl[0], 0xFFFFFFFFu, dst);
+        }
+    }
+}
+
 }  // namespace lpb

@@ -831,6 +831,36 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
     }
 }
 
+uint64_t locpir_b200_loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
+{
+    return loc_pir_folded_scratch(Q, R, l, m);
+}
+
+int locpir_b200_loc_pir_folded_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                       const uint32_t* x_slots, const uint32_t* y_slots,
+                                       const int64_t* boxes, const uint32_t* svc_slots,
+                                       const uint32_t* out_slots, uint64_t scratch_first,
+                                       int xor_tree, locpir_b200_gate_op* ops, uint64_t* count)
+{
+    if (!count || !Q || !R || l < 2 || l > 63 || !m || !x_slots || !y_slots || !boxes ||
+        !svc_slots || !out_slots)
+        return LOCPIR_B200_EINVAL;
+    try {
+        std::vector<locpir_b200_gate_op> v;
+        emit_loc_pir_folded(v, Q, R, l, m, x_slots, y_slots, boxes, svc_slots, out_slots,
+                            scratch_first, xor_tree);
+        if (ops) {
+            if (*count < v.size())
+                return LOCPIR_B200_EINVAL;
+            std::copy(v.begin(), v.end(), ops);
+        }
+        *count = v.size();
+        return LOCPIR_B200_OK;
+    } catch (...) {
+        return LOCPIR_B200_EINVAL;
+    }
+}
+
 int locpir_b200_loc_pir(locpir_b200_ctx* c, uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                         const uint32_t* x_slots, const uint32_t* y_slots,
                         const uint32_t* bnd_slots, const uint32_t* svc_slots,

@@ -54,6 +54,8 @@ inline bool gate_form(uint32_t kind, GateForm& f)
     case LOCPIR_B200_XNOR: f = {0xC0000000u, -2, -2}; return true;
     case LOCPIR_B200_NAND: f = {0x20000000u, -1, -1}; return true;
     case LOCPIR_B200_NOR: f = {0xE0000000u, -1, -1}; return true;
+    case LOCPIR_B200_ANDNY: f = {0xE0000000u, -1, 1}; return true;
+    case LOCPIR_B200_ORNY: f = {0x20000000u, -1, 1}; return true;
     default: return false;
     }
 }
@@ -123,7 +125,8 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
             tmps[id].wave_ks = w;
             P.n_ks++;
             rbr[op.out] = rlin[op.out] = w + 1;
-            static const int cidx[] = {0, 1, 2, 3, 6, -1, -1, 7};
+            // counters: ANDNY / ORNY count as AND / OR
+            static const int cidx[] = {0, 1, 2, 3, 6, -1, -1, 7, -1, -1, 0, 1};
             P.counts[cidx[op.kind]]++;
         } else if (op.kind == LOCPIR_B200_MUX) {
             use(op.in0);

@@ -205,6 +205,8 @@ class Context:
 
     @staticmethod
     def ops_array(ops) -> C.Array:
+        if isinstance(ops, C.Array):
+            return ops
         arr = (GateOp * max(1, len(ops)))()
         for i, (k, a, b, c, o) in enumerate(ops):
             arr[i] = GateOp(k, a, b, c, o)
@@ -336,6 +338,26 @@ def loc_pir_program(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slot
     ops = (GateOp * cnt.value)()
     _check(lib().locpir_b200_loc_pir_program(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first,
                                              int(bool(xor_tree)), ops, C.byref(cnt)))
+    return ops
+
+
+def loc_pir_folded_program(Q, R, l, m, x_slots, y_slots, boxes_signed, svc_slots, out_slots,
+                           scratch_first, xor_tree=True):
+    """Flagged mode: loc_pir against PLAINTEXT box boundaries
+    (dataset.hpp:250-253 makes them trivial words), comparators constant-folded.
+    boxes_signed: [R, 4] (x1, x2, y1, y2) signed l-bit grid values."""
+    arrs = [np.ascontiguousarray(v, np.uint32).reshape(-1)
+            for v in (x_slots, y_slots, svc_slots, out_slots)]
+    bx = np.ascontiguousarray(boxes_signed, np.int64).reshape(-1)
+    if bx.size != 4 * R:
+        raise ValueError("boxes_signed must hold R x 4 values")
+    bxp = bx.ctypes.data_as(C.POINTER(C.c_int64))
+    cnt = C.c_uint64(0)
+    args = (Q, R, l, m, _u32(arrs[0]), _u32(arrs[1]), bxp, _u32(arrs[2]), _u32(arrs[3]),
+            scratch_first, int(bool(xor_tree)))
+    _check(lib().locpir_b200_loc_pir_folded_program(*args, None, C.byref(cnt)))
+    ops = (GateOp * cnt.value)()
+    _check(lib().locpir_b200_loc_pir_folded_program(*args, ops, C.byref(cnt)))
     return ops
 
 

@@ -88,7 +88,8 @@ class PoolLayout:
         self.scratch = n
         self.inputs_end = self.out.min()
         from ._abi import lib
-        self.total = n + lib().locpir_b200_loc_pir_scratch(Q, R, l, m)
+        self.total = n + max(lib().locpir_b200_loc_pir_scratch(Q, R, l, m),
+                             lib().locpir_b200_loc_pir_folded_scratch(Q, R, l, m))
 
 
 def load_batch(ctx, keys, b: LocPirBatch, lay: PoolLayout, seed: int):
@@ -108,11 +109,26 @@ def load_batch(ctx, keys, b: LocPirBatch, lay: PoolLayout, seed: int):
     ctx.h2d(int(lay.svc.min()), keys.encrypt_bits(sbits.reshape(-1), seed + 2))
 
 
-def program(ctx, b: LocPirBatch, lay: PoolLayout, xor_tree=True):
-    from .engine import loc_pir_program
-    ops = loc_pir_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.bnd, lay.svc, lay.out,
-                          lay.scratch, xor_tree)
-    return ctx.program(ops)
+def signed_boxes(b: LocPirBatch) -> np.ndarray:
+    """[R, 4] signed grid values of the boundaries (the words _bits_signed encodes)."""
+    return b.boxes.astype(np.int64) - (1 << (b.l - 1))
+
+
+def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False):
+    """folded=True: flagged plaintext-boundary mode; not for cfg5,
+    whose boundaries are encrypted."""
+    from .engine import loc_pir_folded_program, loc_pir_program
+    if folded:
+        if b.encrypted_bounds:
+            raise ValueError("constant folding needs plaintext boundaries")
+        return loc_pir_folded_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, signed_boxes(b),
+                                      lay.svc, lay.out, lay.scratch, xor_tree)
+    return loc_pir_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.bnd, lay.svc, lay.out,
+                           lay.scratch, xor_tree)
+
+
+def program(ctx, b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False):
+    return ctx.program(program_ops(b, lay, xor_tree, folded))
 
 
 def read_results(ctx, keys, b: LocPirBatch, lay: PoolLayout) -> np.ndarray:

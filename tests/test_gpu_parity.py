@@ -448,3 +448,24 @@ def test_loc_pir_c_abi_entry(dev):
     W.load_batch(ctx, keys, b, lay, seed=78)
     ctx.loc_pir(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.bnd, lay.svc, lay.out, lay.scratch)
     assert np.array_equal(W.read_results(ctx, keys, b, lay), b.truth())
+
+
+@pytest.mark.parametrize("level,Q,R,l,m", [(128, 4, 9, 16, 8), (80, 3, 5, 13, 4)])
+def test_folded_loc_pir_encrypted(dev, level, Q, R, l, m):
+    """Flagged plaintext-boundary mode run encrypted: same decrypted
+    result as the reference circuit, fewer bootstraps."""
+    from paper_2407_19871_b200 import workloads as W
+    p, keys, ctx = dev[level]
+    b = W.make_batch(Q, R, l, m, seed=11 + level)
+    for q in range(min(Q, R)):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    lay = W.PoolLayout(b)
+    ctx.pool_reserve(lay.total)
+    W.load_batch(ctx, keys, b, lay, seed=12)
+    ctx.counters_reset()
+    prog = W.program(ctx, b, lay, folded=True)
+    prog.launch()
+    assert np.array_equal(W.read_results(ctx, keys, b, lay), b.truth())
+    assert ctx.counters()["bootstrap_units"] < b.units() // 2
+    prog.close()
