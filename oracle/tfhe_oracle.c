@@ -237,13 +237,25 @@ void or_fft_tables(uint32_t N, double* W, double* TW, double* UT)
         W[2 * (k + Q)] = -im;
         W[2 * (k + Q) + 1] = re;
     }
+    /* twist psi^j (psi = e^{i pi / N}) in the factored form the GPU forms on the fly
+     * (kernels.cuh, TWIST_CONST): TW[j] = cmul(psi^(j mod 64), psi^(j - j mod 64)) with
+     * both factors rounded first; the untwist is conj(TW[j]) / M (exact scaling). */
     for (uint32_t j = 0; j < M; j++) {
-        double re = j == 0 ? 1.0 : cos(pi * (double)j / (double)N);
-        double im = j == 0 ? 0.0 : sin(pi * (double)j / (double)N);
-        TW[2 * j] = re;
-        TW[2 * j + 1] = im;
-        UT[2 * j] = re / (double)M;
-        UT[2 * j + 1] = -im / (double)M;
+        TW[2 * j] = j == 0 ? 1.0 : cos(pi * (double)j / (double)N);
+        TW[2 * j + 1] = j == 0 ? 0.0 : sin(pi * (double)j / (double)N);
+    }
+    for (uint32_t j = M; j-- > 0;) { /* descending: factors j & 63, j & ~63 are still exact */
+        const uint32_t lo = j & 63u, hi = j & ~63u;
+        if (lo && hi) {
+            const double xr = TW[2 * lo], xi = TW[2 * lo + 1];
+            const double wr = TW[2 * hi], wi = TW[2 * hi + 1];
+            TW[2 * j] = fma(xr, wr, -(xi * wi));
+            TW[2 * j + 1] = fma(xr, wi, xi * wr);
+        }
+    }
+    for (uint32_t j = 0; j < M; j++) {
+        UT[2 * j] = TW[2 * j] / (double)M;
+        UT[2 * j + 1] = -TW[2 * j + 1] / (double)M;
     }
 }
 

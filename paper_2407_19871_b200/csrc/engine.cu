@@ -173,12 +173,21 @@ void make_tables(uint32_t N, std::vector<double2>& W, std::vector<double2>& TW,
         W[k] = make_double2(re, im);
         W[k + Q] = make_double2(-im, re);
     }
-    for (uint32_t j = 0; j < M; j++) {
-        const double re = j == 0 ? 1.0 : std::cos(pi * (double)j / (double)N);
-        const double im = j == 0 ? 0.0 : std::sin(pi * (double)j / (double)N);
-        TW[j] = make_double2(re, im);
-        UT[j] = make_double2(re / (double)M, -im / (double)M);
+    // twist psi^j in factored form: TW[j] = cmul(psi^(j mod 64), psi^(j - j mod 64)), the
+    // product k_blind_rotate forms on the fly (TWIST_CONST); same table as the oracle's
+    // (tfhe_oracle.c or_fft_tables)
+    for (uint32_t j = 0; j < M; j++)
+        TW[j] = make_double2(j == 0 ? 1.0 : std::cos(pi * (double)j / (double)N),
+                             j == 0 ? 0.0 : std::sin(pi * (double)j / (double)N));
+    for (uint32_t j = M; j-- > 0;) {
+        const uint32_t lo = j & 63u, hi = j & ~63u;
+        if (lo && hi) {
+            const double2 x = TW[lo], w = TW[hi];
+            TW[j] = make_double2(std::fma(x.x, w.x, -(x.y * w.y)), std::fma(x.x, w.y, x.y * w.x));
+        }
     }
+    for (uint32_t j = 0; j < M; j++)
+        UT[j] = make_double2(TW[j].x / (double)M, -TW[j].y / (double)M);
 }
 
 void need_keys(locpir_b200_ctx* c)
@@ -447,6 +456,12 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
         CK(cudaMemcpy(c->W.p, W.data(), W.size() * sizeof(double2), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c->TW.p, TW.data(), TW.size() * sizeof(double2), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(c->UT.p, UT.data(), UT.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        {
+            double2 twq[8];
+            for (int q = 0; q < 8; q++)
+                twq[q] = TW[64 * q];
+            CK(cudaMemcpyToSymbol(c_twq, twq, sizeof(twq)));
+        }
         CK(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(KS_CT * p->N * sizeof(uint16_t))));
         CK(cudaFuncSetAttribute(k_blind_rotate_w<3, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -87,6 +87,11 @@ constexpr int MAX_N = 1023;
 #ifndef TWIST_REGS
 #define TWIST_REGS 0
 #endif
+// TWIST_CONST: twist factor psi^(t + 64 q) = cmul(psi^t, psi^(64 q)) formed on the fly from
+// a per-thread register and a __constant__ table (trades shared-memory reads for FP64)
+#ifndef TWIST_CONST
+#define TWIST_CONST 1
+#endif
 #ifndef BK_EVICT_LAST
 #define BK_EVICT_LAST 1
 #endif
@@ -189,6 +194,8 @@ __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
     acc.y = im;
 }
 
+__constant__ double2 c_twq[8];  // psi^(64 q), q = 0..7 (TWIST_CONST)
+
 template <int L, int BGBIT>
 __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     k_blind_rotate(DevParams dp, const BrItem* __restrict__ items,
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     // exchange tiles: [0],[1] cross-warp (alternating), [2] intra-warp
     __shared__ __align__(16) double2 xbuf[3][XTILE];
     __shared__ uint16_t abar[MAX_N + 1];
-#if !TWIST_REGS && !TWIST_TMEM
+#if !TWIST_REGS && !TWIST_TMEM && !TWIST_CONST
     __shared__ __align__(16) double2 tws[FFT_M];  // twist table psi^j
 #endif
 #if TWIST_TMEM
@@ -227,6 +234,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         tmem_st32(ttw, v);
         tmem_wait_st();
     }
+#elif TWIST_CONST
+    const double2 twt = TW[t];
+#define TWIST(q) cmul(twt, c_twq[q])
 #elif TWIST_REGS
     double2 twr[8];  // this thread's twist factors psi^j, j = t + 64 q (untwist = conj / 512)
 #pragma unroll
