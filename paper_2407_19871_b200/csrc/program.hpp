@@ -60,25 +60,56 @@ inline bool gate_form(uint32_t kind, GateForm& f)
     }
 }
 
+// Per-slot scheduling state: ready waves for BR / linear use and read/write flags.
+struct SlotInfo {
+    uint32_t rbr = 0, rlin = 0;
+    uint8_t written = 0, read = 0;
+};
+
+// Dense table when slot ids are proportional to the program size (pool layouts always
+// are), hash map otherwise -- planning 65,536 gates drops from ~35 ms to ~2 ms.
+class SlotTable {
+  public:
+    SlotTable(const locpir_b200_gate_op* ops, uint64_t count)
+    {
+        uint64_t mx = 0;
+        for (uint64_t g = 0; g < count; g++)
+            for (uint32_t s : {ops[g].in0, ops[g].in1, ops[g].in2, ops[g].out})
+                if (s != SLOT_NONE && s > mx)
+                    mx = s;
+        if (mx < 8 * count + (1u << 16))
+            dense_.resize(mx + 1);
+    }
+    SlotInfo& operator[](uint32_t s) { return dense_.empty() ? sparse_[s] : dense_[s]; }
+    uint32_t rbr(uint32_t s) const { return find(s).rbr; }
+    uint32_t rlin(uint32_t s) const { return find(s).rlin; }
+
+  private:
+    const SlotInfo& find(uint32_t s) const
+    {
+        static const SlotInfo none;
+        if (!dense_.empty())
+            return dense_[s];
+        auto it = sparse_.find(s);
+        return it == sparse_.end() ? none : it->second;
+    }
+    std::vector<SlotInfo> dense_;
+    std::unordered_map<uint32_t, SlotInfo> sparse_;
+};
+
 inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
 {
     Plan P;
-    std::unordered_map<uint32_t, uint32_t> rbr, rlin;  // ready wave for BR / linear use
-    std::unordered_set<uint32_t> written, readset;
+    SlotTable st(ops, count);
     struct Tmp {
         uint32_t wave_br;
         uint32_t wave_ks = 0;
     };
     std::vector<Tmp> tmps;
+    tmps.reserve(count);
     // temporary ids (N-dim values) referenced by BR out / KS in until slots are assigned
-    auto ready_br = [&](uint32_t s) {
-        auto it = rbr.find(s);
-        return it == rbr.end() ? 0u : it->second;
-    };
-    auto ready_lin = [&](uint32_t s) {
-        auto it = rlin.find(s);
-        return it == rlin.end() ? 0u : it->second;
-    };
+    auto ready_br = [&](uint32_t s) { return st.rbr(s); };
+    auto ready_lin = [&](uint32_t s) { return st.rlin(s); };
     auto ensure = [&](uint32_t w) {
         if (P.br.size() <= w) {
             P.br.resize(w + 1);
@@ -89,18 +120,19 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
     auto use = [&](uint32_t s) {
         if (s == SLOT_NONE)
             throw std::invalid_argument("gate operand slot missing");
-        readset.insert(s);
+        st[s].read = 1;
     };
     auto def = [&](uint32_t s) {
         if (s == SLOT_NONE)
             throw std::invalid_argument("gate output slot missing");
-        if (written.count(s))
+        SlotInfo& si = st[s];
+        if (si.written)
             throw std::invalid_argument("slot " + std::to_string(s) +
                                         " written twice in one program");
-        if (readset.count(s))
+        if (si.read)
             throw std::invalid_argument("slot " + std::to_string(s) +
                                         " written after being read in the same program");
-        written.insert(s);
+        si.written = 1;
     };
     auto new_br = [&](uint32_t w, uint32_t in0, uint32_t in1, int32_t c0, int32_t c1,
                       uint32_t off) {
@@ -124,7 +156,7 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
             P.ks[w].push_back({id, SLOT_NONE, 0u, op.out});
             tmps[id].wave_ks = w;
             P.n_ks++;
-            rbr[op.out] = rlin[op.out] = w + 1;
+            st[op.out].rbr = st[op.out].rlin = w + 1;
             // counters: ANDNY / ORNY count as AND / OR
             static const int cidx[] = {0, 1, 2, 3, 6, -1, -1, 7, -1, -1, 0, 1};
             P.counts[cidx[op.kind]]++;
@@ -142,7 +174,7 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
             P.ks[w].push_back({t1, t2, 0x20000000u, op.out});
             tmps[t1].wave_ks = tmps[t2].wave_ks = w;
             P.n_ks++;
-            rbr[op.out] = rlin[op.out] = w + 1;
+            st[op.out].rbr = st[op.out].rlin = w + 1;
             P.counts[5]++;
         } else if (op.kind == LOCPIR_B200_NOT || op.kind == LOCPIR_B200_COPY) {
             use(op.in0);
@@ -150,16 +182,16 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
             const uint32_t w = ready_lin(op.in0);
             ensure(w);
             P.lin[w].push_back({op.kind == LOCPIR_B200_NOT ? 0u : 1u, op.in0, op.out, 0});
-            rbr[op.out] = w;
-            rlin[op.out] = w + 1;
+            st[op.out].rbr = w;
+            st[op.out].rlin = w + 1;
             if (op.kind == LOCPIR_B200_NOT)
                 P.counts[4]++;
         } else if (op.kind == LOCPIR_B200_CONST) {
             def(op.out);
             ensure(0);
             P.lin[0].push_back({2u, op.in0 ? 0x20000000u : 0xE0000000u, op.out, 0});
-            rbr[op.out] = 0;
-            rlin[op.out] = 1;
+            st[op.out].rbr = 0;
+            st[op.out].rlin = 1;
         } else {
             throw std::invalid_argument("unknown gate kind " + std::to_string(op.kind));
         }
