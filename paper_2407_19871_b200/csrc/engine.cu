@@ -124,6 +124,8 @@ struct locpir_b200_ctx {
     int small_levels = 1;
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
     DevBuf<uint32_t> ks_partial;
+    DevBuf<uint32_t> h2d_stage;  // packed rows for 1-D host copies (k_repack_rows)
+    DevBuf<uint32_t> d2h_stage;  // packed rows for 1-D device-to-host copies (k_pack_rows)
 };
 
 namespace {
@@ -416,12 +418,26 @@ void pool_copy(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_
     if (!count)
         return;
     const size_t wb = (size_t)(c->p.n + 1) * 4, pb = (size_t)c->dp.n_stride * 4;
-    if (to_pool)
+    if (to_pool && kind == cudaMemcpyHostToDevice && count >= 256) {
+        // one 1-D copy into a packed staging buffer + an HBM-speed repack kernel
+        c->h2d_stage.reserve((size_t)count * (c->p.n + 1), c->stream, false);
+        CK(cudaMemcpyAsync(c->h2d_stage.p, src, (size_t)count * wb, kind, c->stream));
+        k_repack_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(c->dp, c->h2d_stage.p, count,
+                                                             c->pool_n.p + first * c->dp.n_stride);
+        CK(cudaGetLastError());
+    } else if (to_pool) {
         CK(cudaMemcpy2DAsync(c->pool_n.p + first * c->dp.n_stride, pb, src, wb, wb, count, kind,
                              c->stream));
-    else
+    } else if (kind == cudaMemcpyDeviceToHost && count >= 256) {
+        c->d2h_stage.reserve((size_t)count * (c->p.n + 1), c->stream, false);
+        k_pack_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(c->dp, c->pool_n.p + first * c->dp.n_stride,
+                                                           count, c->d2h_stage.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(dst, c->d2h_stage.p, (size_t)count * wb, kind, c->stream));
+    } else {
         CK(cudaMemcpy2DAsync(dst, wb, c->pool_n.p + first * c->dp.n_stride, pb, wb, count, kind,
                              c->stream));
+    }
 }
 
 }  // namespace

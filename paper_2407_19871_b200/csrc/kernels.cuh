@@ -98,6 +98,9 @@ constexpr int MAX_N = 1023;
 #ifndef TWIST_TMEM
 #define TWIST_TMEM 0
 #endif
+#ifndef BK_RELAXED
+#define BK_RELAXED 1
+#endif
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 2
 #endif
@@ -169,7 +172,16 @@ __device__ __forceinline__ double2 untwist(double2 tw)
 __device__ __forceinline__ double2 ld_stream(const double2* p)
 {
     double2 v;
-#if BK_EVICT_LAST
+#if BK_RELAXED
+    // a relaxed gpu-scope load may not be sunk below the FFT's bar.sync by ptxas (a weak
+    // .nc load is, which turns the prefetch into a stall at the MAC)
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "ld.relaxed.gpu.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
+        : "=d"(v.x), "=d"(v.y)
+        : "l"(p));
+#elif BK_EVICT_LAST
     asm volatile(
         "{\n\t.reg .b64 pol;\n\t"
         "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
@@ -413,6 +425,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 // warp (all lanes work on the same ciphertext), so the row choice is a
 // warp-uniform branch and each selected row costs one add per column.
 // ---------------------------------------------------------------------------
+#ifndef KS_PREFETCH
+#define KS_PREFETCH 1
+#endif
 #ifndef KS_MINB
 #define KS_MINB 4
 #endif
@@ -474,6 +489,9 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
     const size_t row_stride = dp.n_stride;
     const uint4* base = reinterpret_cast<const uint4*>(ksk + col);
     const size_t rs4 = row_stride / 4;
+#if KS_PREFETCH
+    uint4 n1 = __ldg(base), n2 = __ldg(base + rs4), n3 = __ldg(base + 2 * rs4);
+#endif
     for (uint32_t i = 0; i < N; i++) {
         uint32_t dw[KS_CT / 2];
         const uint32_t* dp32 = reinterpret_cast<const uint32_t*>(dig + i * KS_CT);
@@ -482,8 +500,20 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
             dw[c] = dp32[c];  // broadcast: two ciphertexts' digit words
 #pragma unroll
         for (int j = 0; j < 8; j++) {
+#if KS_PREFETCH
+            // rows of step (i, j) were loaded one step ahead; issue step (i, j+1) now
+            const uint4 r1 = n1, r2 = n2, r3 = n3;
+            {
+                const uint32_t ni = j == 7 ? min(i + 1, N - 1) : i;
+                const uint4* rn = base + ((size_t)ni * 24 + ((j + 1) & 7) * 3) * rs4;
+                n1 = __ldg(rn);
+                n2 = __ldg(rn + rs4);
+                n3 = __ldg(rn + 2 * rs4);
+            }
+#else
             const uint4* rj = base + ((size_t)i * 24 + j * 3) * rs4;
             const uint4 r1 = __ldg(rj), r2 = __ldg(rj + rs4), r3 = __ldg(rj + 2 * rs4);
+#endif
 #pragma unroll
             for (int c = 0; c < KS_CT; c++) {
                 const uint32_t w = dw[c >> 1] >> ((c & 1) * 16);
@@ -528,6 +558,34 @@ __global__ void k_linear(DevParams dp, const LinItem* __restrict__ items, uint32
                 v = 0u - v;
         }
         pool_n[(size_t)it.out * dp.n_stride + w] = v;
+    }
+}
+
+// Host-to-pool repack: packed wire rows (n+1 words) staged by one 1-D copy -> pitched pool
+// rows.  A pinned 2-D copy with a 2,524 B row / 2,528 B pitch runs at ~19 GB/s on the
+// B200 host link against ~55 GB/s for the 1-D copy (tools/copy_bench.py).
+__global__ void k_repack_rows(DevParams dp, const uint32_t* __restrict__ packed, uint64_t count,
+                              uint32_t* __restrict__ pool_rows)
+{
+    const uint32_t words = dp.n + 1;
+    const uint64_t total = count * words;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = e / words, w = e - g * words;
+        pool_rows[g * dp.n_stride + w] = packed[e];
+    }
+}
+
+// Pool-to-host pack: pitched pool rows -> packed wire rows for one 1-D device-to-host copy.
+__global__ void k_pack_rows(DevParams dp, const uint32_t* __restrict__ pool_rows, uint64_t count,
+                            uint32_t* __restrict__ packed)
+{
+    const uint32_t words = dp.n + 1;
+    const uint64_t total = count * words;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = e / words, w = e - g * words;
+        packed[e] = pool_rows[g * dp.n_stride + w];
     }
 }
 

@@ -2,9 +2,13 @@
 pitch) against a plain 1-D copy of the same bytes, pinned host memory, and the host-side
 planning cost of a 65,536-gate batch."""
 import ctypes as C
+import os
+import sys
 import time
 
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 from paper_2407_19871_b200 import Context, TfheParams, _abi
 from paper_2407_19871_b200.engine import plan
