@@ -469,3 +469,21 @@ def test_folded_loc_pir_encrypted(dev, level, Q, R, l, m):
     assert np.array_equal(W.read_results(ctx, keys, b, lay), b.truth())
     assert ctx.counters()["bootstrap_units"] < b.units() // 2
     prog.close()
+
+
+@pytest.mark.parametrize("count,first", [(1000, 7), (255, 3), (256, 0), (4097, 1)])
+def test_pool_transfer_round_trip(dev, count, first):
+    """Host<->pool copies: >= 256 rows go as one 1-D copy + repack/pack kernels (K4),
+    fewer as a pitched 2-D copy; both must round-trip the wire layout exactly and leave
+    neighbouring slots untouched."""
+    p, keys, ctx = dev[128]
+    ctx.pool_reserve(first + count + 2)
+    rng = np.random.default_rng(count)
+    guard = rng.integers(0, 2 ** 32, (first + count + 2, p.n + 1), dtype=np.uint64).astype(np.uint32)
+    ctx.h2d(0, guard)
+    rows = rng.integers(0, 2 ** 32, (count, p.n + 1), dtype=np.uint64).astype(np.uint32)
+    ctx.h2d(first, rows)
+    back = ctx.d2h(0, first + count + 2)
+    assert np.array_equal(back[first:first + count], rows)
+    assert np.array_equal(back[:first], guard[:first])
+    assert np.array_equal(back[first + count:], guard[first + count:])
