@@ -155,6 +155,19 @@ def cpu_oracle_rate(budget_s=12.0, threads=None, seed=KEY_SEED):
                       f"{threads} threads, {dt:.1f} s)", "correct": bool(ok)}
 
 
+def host_cpu():
+    """CPU model and core count of the box the baseline ran on."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 def standin_rate(threads=None):
     """The reference's own gate refresh stand-in (compiled read-only into oracle/_ref)."""
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
@@ -170,6 +183,32 @@ def standin_rate(threads=None):
                          "hom_not(hom_and) with a secret-key re-encryption per gate"}
     except Exception as e:  # pragma: no cover
         return {"error": str(e)}
+
+
+def standin_locpir_rates(threads=None):
+    """The reference's own loc_pir (circuits.hpp:276-324) under its refresh-oracle engine on
+    its synthetic case at each LocPIR config's shape (compiled read-only into oracle/_ref)."""
+    from paper_2407_19871_b200 import workloads as W
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    if not os.path.exists(exe):
+        return None
+    threads = threads or os.cpu_count() or 1
+    out = {"label": "functional stand-in, no bootstrapping (gate_engine.hpp:117-123): every "
+                    "gate is a secret-key re-encryption, ~1e3-1e4x cheaper than a bootstrap; "
+                    "reference parameter sets sec80/sec128", "cores": threads, "configs": {}}
+    for name, (sec, Qfull, R, l, m, enc) in W.CONFIGS.items():
+        q = {"cfg1": 200, "cfg3": 2, "cfg4": 50, "cfg5": 8}.get(name, 4)
+        try:
+            r = subprocess.run([exe, "standin_locpir", str(R), str(l), str(m), str(sec), str(q),
+                                str(threads)], capture_output=True, text=True, timeout=300)
+            d = json.loads(r.stdout)
+            out["configs"][name] = {"queries_per_s": d["queries_per_s"], "queries": q,
+                                    "correct": d["wrong"] == 0,
+                                    "boundaries": "trivial (the reference encodes regions as "
+                                                  "constants)" if enc else "trivial"}
+        except Exception as e:  # pragma: no cover
+            out["configs"][name] = {"error": str(e)}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -201,6 +240,62 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# CPU baseline for the LocPIR configs: (queries, boxes) actually evaluated by the oracle port
+CPU_LOCPIR_SAMPLES = {"cfg1": (1, None), "cfg3": (1, 8), "cfg4": (1, 8), "cfg5": (1, 4)}
+
+
+def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
+    """The same loc_pir gate programs evaluated by the oracle port (FP64-FFT mode) level by
+    level on all host threads (oracle.run_program), decrypted and checked against the
+    plaintext answer.  cfg1 runs in full; cfg3/4/5 run on a box subsample and are
+    extrapolated linearly in bootstrap units (SURVEY §8(d) "run cfg3/4/5 on a stated
+    subsample and extrapolate linearly")."""
+    from oracle import oracle as O
+    from paper_2407_19871_b200 import workloads as W
+    threads = threads or os.cpu_count() or 1
+    out = {}
+    keys = {}
+    for name, (sec, Qfull, Rfull, l, m, enc) in W.CONFIGS.items():
+        Qs, Rs = CPU_LOCPIR_SAMPLES[name]
+        Rs = Rs or Rfull
+        if sec not in keys:
+            keys[sec] = O.TfheKeys(sec, seed)
+        K = keys[sec]
+        b = W.make_batch(Qs, Rs, l, m, seed=seed + 31 + len(out), encrypted_bounds=enc)
+        b.x[0] = (b.boxes[0, 0] + b.boxes[0, 1]) // 2
+        b.y[0] = (b.boxes[0, 2] + b.boxes[0, 3]) // 2
+        lay = W.PoolLayout(b)
+        pool = np.zeros((lay.total, K.n + 1), np.uint32)
+        smp = O.NoiseSampler(seed + 7, K.p.alpha_in)
+        enc_bits = lambda bits: np.stack([O.encrypt_bit(int(v), K.lwe_key, smp) for v in bits])
+        qbits = np.concatenate([W._bits_signed(b.x, l).reshape(-1), W._bits_signed(b.y, l).reshape(-1)])
+        pool[lay.x.reshape(-1)] = enc_bits(qbits[: Qs * l])
+        pool[lay.y.reshape(-1)] = enc_bits(qbits[Qs * l:])
+        bbits = W._bits_signed(b.boxes, l).reshape(-1)
+        if enc:
+            pool[lay.bnd.reshape(-1)] = enc_bits(bbits)
+        else:  # trivial words (dataset.hpp:250-253)
+            pool[lay.bnd.reshape(-1), K.n] = np.where(bbits == 1, 0x20000000, 0xE0000000)
+        sbits = ((b.payload[:, None] >> np.arange(m, dtype=np.uint64)) & 1).astype(np.uint8)
+        pool[lay.svc.reshape(-1)] = enc_bits(sbits.reshape(-1))
+        ops = W.program_ops(b, lay)
+        t = time.perf_counter()
+        O.run_program(K, ops, pool, threads)
+        dt = time.perf_counter() - t
+        got = np.array([sum(O.decrypt_bit(pool[lay.out[q, j]], K.lwe_key) << j for j in range(m))
+                        for q in range(Qs)], np.uint64)
+        units = b.units()
+        full_units = Qfull * Rfull * (12 * l + 2 * m + 3)
+        out[name] = {
+            "queries_per_s": Qs / dt if Rs == Rfull else (units / dt) / (full_units / Qfull),
+            "units_per_s": units / dt, "seconds": dt, "correct": bool(np.array_equal(got, b.truth())),
+            "sample": (f"{Qs} query, all {Rfull} boxes, measured" if Rs == Rfull else
+                       f"{Qs} query x {Rs} of {Rfull} boxes measured, queries/s extrapolated "
+                       f"linearly in bootstrap units"),
+        }
+    return {"kind": "port", "cores": threads, "unit": "queries/s", "configs": out}
 
 
 # ---------------------------------------------------------------------------
@@ -401,7 +496,11 @@ def run_b200(args):
             line["locpir"] = locpir_results
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_oracle_rate(budget_s=args.ref_budget)
+            line["cpu_baseline"]["host_cpu"] = host_cpu()
             line["reference_standin"] = standin_rate()
+            if not args.no_locpir:
+                line["cpu_baseline_locpir"] = cpu_locpir_baseline()
+                line["reference_standin_locpir"] = standin_locpir_rates()
         print(json.dumps(line), flush=True)
     prog.close()
     ctx.close()

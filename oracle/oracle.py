@@ -19,7 +19,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
 
 EXACT, FFT = 0, 1
-GATES = {"and": 0, "or": 1, "xor": 2, "xnor": 3, "nand": 4, "mux": 5, "not": 6, "nor": 7}
+GATES = {"and": 0, "or": 1, "xor": 2, "xnor": 3, "nand": 4, "mux": 5, "not": 6, "nor": 7,
+         "andny": 10, "orny": 11}
+
+
+class GateItem(C.Structure):
+    _fields_ = [("kind", C.c_int), ("a", C.c_void_p), ("b", C.c_void_p), ("c", C.c_void_p),
+                ("out", C.c_void_p)]
 
 
 class Params(C.Structure):
@@ -86,6 +92,8 @@ def lib():
         L.or_external_product.argtypes = [C.POINTER(KeySet), C.c_uint32, u32p, C.c_int, u32p]
         L.or_keyswitch.argtypes = [C.POINTER(KeySet), u32p, u32p]
         L.or_gate.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_int, u32p]
+        L.or_gate_list.argtypes = [C.POINTER(KeySet), C.POINTER(GateItem), C.c_uint64, C.c_int,
+                                   C.c_int]
         L.or_gate_batch.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_uint64,
                                     C.c_int, C.c_int]
         _lib = L
@@ -280,3 +288,52 @@ class TfheKeys:
         out = np.zeros(self.N, np.int32)
         lib().or_decompose(C.byref(self.p), _u32(x), level, out.ctypes.data)
         return out
+
+
+# gate-program kinds (include/locpir_b200.h) -> oracle kinds; NOT/COPY/CONST are free
+_PROG_BOOT = {0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5, 7: 7, 10: 10, 11: 11}
+_NOT, _COPY, _CONST = 6, 8, 9
+
+
+def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: int = FFT):
+    """Evaluates a gate program (5-tuples or ctypes GateOps over pool slots, the layout of
+    include/locpir_b200.h) on the oracle: bootstrapped gates level by level, each level
+    one threaded or_gate_list call; free gates in program order between levels.
+    pool: [slots, n+1] uint32, updated in place.  Test / baseline infrastructure."""
+    SLOT_NONE = 0xFFFFFFFF
+    ops = [(o.kind, o.in0, o.in1, o.in2, o.out) if not isinstance(o, tuple) else o for o in ops]
+    lvl = {}
+    levels = {}
+    for i, (k, a, b, c, o) in enumerate(ops):
+        ins = [s for s in (a, b, c) if s != SLOT_NONE] if k != _CONST else []
+        base = max((lvl.get(s, 0) for s in ins), default=0)
+        L = base + 1 if k in _PROG_BOOT else base
+        lvl[o] = L
+        levels.setdefault(L, []).append(i)
+    row = pool.strides[0]
+    base_ptr = pool.ctypes.data
+    n = pool.shape[1] - 1
+    for L in sorted(levels):
+        idx = levels[L]
+        boot = [i for i in idx if ops[i][0] in _PROG_BOOT]
+        if boot:
+            items = (GateItem * len(boot))()
+            for j, i in enumerate(boot):
+                k, a, b, c, o = ops[i]
+                items[j] = GateItem(_PROG_BOOT[k], base_ptr + a * row,
+                                    base_ptr + b * row if b != SLOT_NONE else None,
+                                    base_ptr + c * row if c != SLOT_NONE else None,
+                                    base_ptr + o * row)
+            rc = lib().or_gate_list(C.byref(K.ks), items, len(boot), mode, threads)
+            if rc:
+                raise ValueError(f"oracle gate list failed: {rc}")
+        for i in idx:
+            k, a, b, c, o = ops[i]
+            if k == _NOT:
+                pool[o] = (0 - pool[a].astype(np.int64)) & 0xFFFFFFFF
+            elif k == _COPY:
+                pool[o] = pool[a]
+            elif k == _CONST:
+                pool[o] = 0
+                pool[o, n] = 0x20000000 if a else 0xE0000000
+    return pool

@@ -223,8 +223,35 @@ static int standin(uint64_t gates, unsigned threads)
     return bad ? 1 : 0;
 }
 
+// Times the reference loc_pir (circuits.hpp:276-324) under the refresh-oracle engine on
+// the reference's synthetic case (bench.hpp:150-189) with `threads` region workers.
+static int standin_locpir(uint32_t N, uint8_t l, uint32_t m, int sec, uint32_t queries,
+                          unsigned threads)
+{
+    const TlweParams p = sec == 80 ? TlweParams::sec80() : TlweParams::sec128();
+    GateEngine eng = GateEngine::make_tlwe_oracle(keygen(p, 1), 2);
+    auto c = detail::synthetic_case(N, l, m, eng, nullptr, nullptr);
+    uint64_t wrong = 0;
+    auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t q = 0; q < queries; q++) {
+        auto out = loc_pir(c.x, c.y, c.regions, eng, threads);
+        wrong += decrypt_service(out, eng) != c.expected;
+    }
+    double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::printf("{\"queries\": %u, \"threads\": %u, \"seconds\": %.6f, \"queries_per_s\": %.6f, "
+                "\"wrong\": %llu}\n",
+                queries, threads, secs, queries / secs, (unsigned long long)wrong);
+    return wrong ? 1 : 0;
+}
+
 int main(int argc, char** argv)
 {
+    if (argc >= 8 && std::strcmp(argv[1], "standin_locpir") == 0)
+        return standin_locpir((uint32_t)std::strtoul(argv[2], nullptr, 10),
+                              (uint8_t)std::strtoul(argv[3], nullptr, 10),
+                              (uint32_t)std::strtoul(argv[4], nullptr, 10), std::atoi(argv[5]),
+                              (uint32_t)std::strtoul(argv[6], nullptr, 10),
+                              (unsigned)std::strtoul(argv[7], nullptr, 10));
     if (argc >= 2 && std::strcmp(argv[1], "golden") == 0)
         return golden();
     if (argc >= 2 && std::strcmp(argv[1], "standin") == 0) {
@@ -233,6 +260,7 @@ int main(int argc, char** argv)
                                      : std::max(1u, std::thread::hardware_concurrency());
         return standin(gates, threads);
     }
-    std::fprintf(stderr, "usage: ref_driver golden | standin [gates] [threads]\n");
+    std::fprintf(stderr, "usage: ref_driver golden | standin [gates] [threads] | "
+                         "standin_locpir N l m sec queries threads\n");
     return 2;
 }

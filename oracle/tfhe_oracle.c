@@ -717,6 +717,8 @@ int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
     case OR_GATE_XNOR: lin2(n, 0xC0000000u, -2, a, -2, b, comb); break;
     case OR_GATE_NAND: lin2(n, 0x20000000u, -1, a, -1, b, comb); break;
     case OR_GATE_NOR: lin2(n, 0xE0000000u, -1, a, -1, b, comb); break;
+    case OR_GATE_ANDNY: lin2(n, 0xE0000000u, -1, a, 1, b, comb); break;
+    case OR_GATE_ORNY: lin2(n, 0x20000000u, -1, a, 1, b, comb); break;
     case OR_GATE_NOT:
         for (uint32_t q = 0; q <= n; q++)
             out[q] = 0u - a[q];
@@ -790,6 +792,57 @@ int or_gate_batch(const or_keyset* ks, int kind, const uint32_t* a, const uint32
     for (int w = 1; w < threads; w++)
         pthread_create(&tid[w], NULL, batch_worker, &jobs[w]);
     batch_worker(&jobs[0]);
+    int rc = jobs[0].rc;
+    for (int w = 1; w < threads; w++) {
+        pthread_join(tid[w], NULL);
+        if (jobs[w].rc)
+            rc = jobs[w].rc;
+    }
+    free(jobs);
+    free(tid);
+    return rc;
+}
+
+typedef struct {
+    const or_keyset* ks;
+    const or_gate_item* items;
+    int mode;
+    uint64_t lo, hi;
+    int rc;
+} list_job;
+
+static void* list_worker(void* arg)
+{
+    list_job* j = (list_job*)arg;
+    for (uint64_t g = j->lo; g < j->hi; g++) {
+        const or_gate_item* it = &j->items[g];
+        int rc = or_gate(j->ks, it->kind, it->a, it->b, it->c, j->mode, it->out);
+        if (rc)
+            j->rc = rc;
+    }
+    return NULL;
+}
+
+int or_gate_list(const or_keyset* ks, const or_gate_item* items, uint64_t count, int mode,
+                 int threads)
+{
+    if (threads < 1)
+        threads = 1;
+    if ((uint64_t)threads > count)
+        threads = count ? (int)count : 1;
+    list_job* jobs = (list_job*)calloc(threads, sizeof(list_job));
+    pthread_t* tid = (pthread_t*)calloc(threads, sizeof(pthread_t));
+    const uint64_t chunk = (count + threads - 1) / threads;
+    for (int w = 0; w < threads; w++) {
+        jobs[w].ks = ks;
+        jobs[w].items = items;
+        jobs[w].mode = mode;
+        jobs[w].lo = (uint64_t)w * chunk < count ? (uint64_t)w * chunk : count;
+        jobs[w].hi = jobs[w].lo + chunk < count ? jobs[w].lo + chunk : count;
+    }
+    for (int w = 1; w < threads; w++)
+        pthread_create(&tid[w], NULL, list_worker, &jobs[w]);
+    list_worker(&jobs[0]);
     int rc = jobs[0].rc;
     for (int w = 1; w < threads; w++) {
         pthread_join(tid[w], NULL);

@@ -142,7 +142,9 @@ enum {
     OR_GATE_NAND = 4,
     OR_GATE_MUX = 5,
     OR_GATE_NOT = 6,
-    OR_GATE_NOR = 7
+    OR_GATE_NOR = 7,
+    OR_GATE_ANDNY = 10, /* AND(NOT a, b): flagged constant-folding mode */
+    OR_GATE_ORNY = 11   /* OR(NOT a, b) */
 };
 /* out = gate(a, b[, c]) ; for MUX: out = a ? b : c.  n-dim in/out. */
 int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
@@ -151,6 +153,16 @@ int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
  * parallel.hpp:15-52).  a,b,out are [count][n+1]. */
 int or_gate_batch(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
                   uint32_t* out, uint64_t count, int mode, int threads);
+
+/* Heterogeneous gate list on `threads` host threads (static block partition as
+ * parallel.hpp:15-52): one level of a gate program. */
+typedef struct {
+    int kind;
+    const uint32_t *a, *b, *c;
+    uint32_t* out;
+} or_gate_item;
+int or_gate_list(const or_keyset* ks, const or_gate_item* items, uint64_t count, int mode,
+                 int threads);
 
 #ifdef __cplusplus
 }
