@@ -311,6 +311,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
     plaintext XOR of the payloads of all containing boxes."""
     import torch
     from paper_2407_19871_b200 import ClientKeys, Context, TfheParams, workloads as W
+    from paper_2407_19871_b200.dist import GpuBackend, ShardedLocPir
     from paper_2407_19871_b200.engine import plan
     out = {}
     ctx80 = keys80 = None
@@ -325,41 +326,56 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
         else:
             ctx, keys = ctx128, keys128
         Q = min(Qfull, LOCPIR_SAMPLES[name])
-        b = W.make_batch(Q, R, l, m, seed=KEY_SEED + 17 * rank + len(out), encrypted_bounds=enc)
-        lay = W.PoolLayout(b)
-        ctx.pool_reserve(lay.total)
-        W.load_batch(ctx, keys, b, lay, seed=5000 + rank)
+        # cfg1 replicas (independent queries per GPU); cfg3 boxes sharded
+        # (partial XOR roots all-gathered, rank-0 combine level); cfg4/cfg5 queries
+        # sharded, results gathered to rank 0.  Every rank builds the same seeded batch.
+        if name == "cfg1":
+            mode, Qb, bseed, world, rk, scaling = "queries", Q, KEY_SEED + 17 * rank, 1, 0, "replicas"
+        elif name == "cfg3":
+            mode, Qb, bseed, world, rk, scaling = "boxes", Q, KEY_SEED + 3, ws, rank, "strong"
+        else:
+            mode, Qb, bseed, world, rk, scaling = "queries", Q * ws, KEY_SEED + 4, ws, rank, "weak"
+        b = W.make_batch(Qb, R, l, m, seed=bseed, encrypted_bounds=enc)
+        for q in range(min(Qb, R)):  # some queries inside boxes
+            b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+            b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+        be = GpuBackend(ctx, keys, torch.device("cuda", local))
         # folded: flagged plaintext-boundary mode, not the reference count
         for folded in ((False, True) if not enc else (False,)):
-            ops = W.program_ops(b, lay, True, folded)
-            units = plan(ops)["blind_rotations"]
-            prog = ctx.program(ops)
-            prog.launch()  # warm-up
+            lay_full = W.PoolLayout(b)
+            units = plan(W.program_ops(b, lay_full, True, folded))["blind_rotations"]
+            run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded)
+            run.launch()  # warm-up
             torch.cuda.synchronize()
             reps = 3 if units < 200000 else 1
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(reps):
-                prog.launch()
+                run.launch()
             e1.record()
             torch.cuda.synchronize()
             ms = max_over_ranks(e0.elapsed_time(e1) / reps)
-            ok = bool(np.array_equal(W.read_results(ctx, keys, b, lay), b.truth()))
+            res = run.results()
+            ok = bool(res is None or np.array_equal(res, b.truth()))
+            qtot = ws * Qb if scaling == "replicas" else Qb
             out[name + ("_folded" if folded else "")] = {
-                "queries_per_s": ws * Q / (ms / 1e3), "ms_per_batch": ms, "queries_per_gpu": Q,
-                "full_batch_queries": Qfull, "boxes": R, "l": l, "m": m, "security_bits": sec,
-                "encrypted_boundaries": enc, "bootstrap_units_per_query": units // Q,
-                "reference_units_per_query": b.units() // Q,
-                "levels_launched": prog.kernels, "units_per_s": ws * units / (ms / 1e3),
-                "correct": ok,
+                "queries_per_s": qtot / (ms / 1e3), "ms_per_batch": ms,
+                "queries_per_batch": qtot, "full_batch_queries": Qfull, "boxes": R, "l": l,
+                "m": m, "security_bits": sec, "encrypted_boundaries": enc,
+                "bootstrap_units_per_query": units // Qb,
+                "reference_units_per_query": b.units() // Qb,
+                "units_per_s": (qtot // Qb) * units / (ms / 1e3), "correct": ok,
+                "sharding": {"cfg1": "replicas", "cfg3": "boxes (partial roots all-gathered, "
+                             "rank-0 combine)"}.get(name, "queries (results gathered to rank 0)"),
+                "scaling": scaling,
                 "mode": ("flagged: plaintext boundaries constant-folded (not the reference "
                          "gate count)") if folded else "reference circuit (N(12l+2m+3) units)",
                 "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
                                                            "(per-query cost is batch-independent "
                                                            "once the GPU is saturated)",
             }
-            prog.close()
+            run.close()
     if ctx80 is not None:
         ctx80.close()
     return out

@@ -168,7 +168,10 @@ int locpir_b200_gate_batch_host(locpir_b200_ctx* ctx, uint32_t kind, const uint3
  *   scratch_first    : first pool slot the circuit may use for intermediates
  *                      (needs locpir_b200_loc_pir_scratch() slots)
  *   xor_tree         : 0 = the reference's N-long XOR chain (circuits.hpp:257-261),
- *                      1 = balanced tree (same N*m XOR count, log2 N depth).
+ *                      1 = balanced tree (same N*m XOR count, log2 N depth),
+ *                      2 = box-sharded partial: tree root copied to out_slots without
+ *                          the final XOR with Enc(0) (N-1 XORs per column); a rank-0
+ *                          combine of the shards' partials restores N*m.
  * Gate counts follow N(12l + 2m + 3) units per query (bench.hpp:35-43). */
 uint64_t locpir_b200_loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m);
 int locpir_b200_loc_pir(locpir_b200_ctx* ctx, uint32_t Q, uint32_t R, uint32_t l, uint32_t m,

@@ -57,6 +57,27 @@ inline uint64_t loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
     return (uint64_t)Q * per_query;
 }
 
+// Balanced XOR tree over one bit column.  mode 1: root XOR Enc(0) -> dst (N XOR units for
+// N boxes, as the reference chain).  mode 2 (box-sharded partial): the root
+// is copied to dst without the XOR with Enc(0) (N-1 units); the rank-0 combine adds one
+// XOR per shard plus the one with Enc(0), so the total stays N units.
+inline void emit_xor_root(Emitter& e, std::vector<uint32_t> lvl, uint32_t zero, uint32_t dst,
+                          int mode)
+{
+    while (lvl.size() > 1) {
+        std::vector<uint32_t> nxt;
+        for (size_t i = 0; i + 1 < lvl.size(); i += 2)
+            nxt.push_back(e.gate(LOCPIR_B200_XOR, lvl[i], lvl[i + 1]));
+        if (lvl.size() & 1)
+            nxt.push_back(lvl.back());
+        lvl.swap(nxt);
+    }
+    if (mode == 2)
+        e.gate(LOCPIR_B200_COPY, lvl[0], 0xFFFFFFFFu, 0xFFFFFFFFu, dst);
+    else
+        e.gate(LOCPIR_B200_XOR, zero, lvl[0], 0xFFFFFFFFu, dst);
+}
+
 // loc_pir (circuits.hpp:276-324) for Q queries.  xor_tree = 0 keeps the
 // reference's N-long chain per bit column (circuits.hpp:257-261); 1 uses a
 // balanced tree of N-1 XORs plus one XOR with Enc(0): still N*m XOR units.
@@ -98,15 +119,7 @@ inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint
                 std::vector<uint32_t> lvl(R);
                 for (uint32_t r = 0; r < R; r++)
                     lvl[r] = masked[(size_t)r * m + j];
-                while (lvl.size() > 1) {
-                    std::vector<uint32_t> nxt;
-                    for (size_t i = 0; i + 1 < lvl.size(); i += 2)
-                        nxt.push_back(e.gate(LOCPIR_B200_XOR, lvl[i], lvl[i + 1]));
-                    if (lvl.size() & 1)
-                        nxt.push_back(lvl.back());
-                    lvl.swap(nxt);
-                }
-                e.gate(LOCPIR_B200_XOR, zero, lvl[0], 0xFFFFFFFFu, dst);
+                emit_xor_root(e, lvl, zero, dst, xor_tree);
             }
         }
     }
@@ -193,15 +206,7 @@ inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t 
                     acc = e.gate(LOCPIR_B200_XOR, acc, lvl[r], 0xFFFFFFFFu, r + 1 == R ? dst : 0xFFFFFFFFu);
                 continue;
             }
-            while (lvl.size() > 1) {
-                std::vector<uint32_t> nxt;
-                for (size_t i = 0; i + 1 < lvl.size(); i += 2)
-                    nxt.push_back(e.gate(LOCPIR_B200_XOR, lvl[i], lvl[i + 1]));
-                if (lvl.size() & 1)
-                    nxt.push_back(lvl.back());
-                lvl.swap(nxt);
-            }
-            e.gate(LOCPIR_B200_XOR, zero, lvl[0], 0xFFFFFFFFu, dst);
+            emit_xor_root(e, lvl, zero, dst, xor_tree);
         }
     }
 }

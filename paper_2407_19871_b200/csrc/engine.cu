@@ -844,7 +844,7 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                 locpir_b200_gate_op* ops, uint64_t* count)
 {
     if (!count || !Q || !R || l < 2 || !m || !x_slots || !y_slots || !bnd_slots || !svc_slots ||
-        !out_slots)
+        !out_slots || xor_tree < 0 || xor_tree > 2)
         return LOCPIR_B200_EINVAL;
     try {
         std::vector<locpir_b200_gate_op> v;
@@ -874,7 +874,7 @@ int locpir_b200_loc_pir_folded_program(uint32_t Q, uint32_t R, uint32_t l, uint3
                                        int xor_tree, locpir_b200_gate_op* ops, uint64_t* count)
 {
     if (!count || !Q || !R || l < 2 || l > 63 || !m || !x_slots || !y_slots || !boxes ||
-        !svc_slots || !out_slots)
+        !svc_slots || !out_slots || xor_tree < 0 || xor_tree > 2)
         return LOCPIR_B200_EINVAL;
     try {
         std::vector<locpir_b200_gate_op> v;
@@ -899,7 +899,7 @@ int locpir_b200_loc_pir(locpir_b200_ctx* c, uint32_t Q, uint32_t R, uint32_t l, 
 {
     return guarded(c, [&] {
         if (!Q || !R || l < 2 || !m || !x_slots || !y_slots || !bnd_slots || !svc_slots ||
-            !out_slots)
+            !out_slots || xor_tree < 0 || xor_tree > 2)
             throw std::invalid_argument("loc_pir: bad arguments");
         if (scratch_first + loc_pir_scratch(Q, R, l, m) > c->pool_slots)
             throw std::invalid_argument("loc_pir: pool too small for the circuit's scratch");

@@ -79,3 +79,151 @@ def gather_to_root(local: "torch.Tensor", total_rows: int, rank: int, world: int
         lo, hi = shard_range(total_rows, r, world)
         out.append(parts[r][:hi - lo])
     return torch.cat(out, 0)
+
+
+def gather_counts_to_root(local: "torch.Tensor", counts: list, rank: int, world: int):
+    """Gathers per-rank row blocks of known sizes `counts[r]` to rank 0 (rows padded to
+    max(counts) for the collective); returns the concatenation on rank 0, None elsewhere."""
+    import torch.distributed as dist
+    if world == 1:
+        return local
+    mx = max(counts)
+    pad = local.new_zeros((mx,) + tuple(local.shape[1:]))
+    pad[:local.shape[0]] = local
+    parts = [pad.new_empty(pad.shape) for _ in range(world)]
+    dist.all_gather(parts, pad)  # NCCL has no gather; gloo takes the same path
+    if rank != 0:
+        return None
+    import torch
+    return torch.cat([parts[r][:counts[r]] for r in range(world)], 0)
+
+
+# ---------------------------------------------------------------------------
+# Sharded LocPIR (SURVEY §8(e)): cfg3 shards BOXES (each rank reduces its boxes to a
+# partial XOR root, rank 0 gathers and combines); cfg4/cfg5 shard QUERIES (results
+# gathered to rank 0).  The flow is written against a small backend so the same code
+# runs on the B200 engine (GpuBackend, NCCL) and, in tests, on a plaintext interpreter
+# over gloo.
+# ---------------------------------------------------------------------------
+class GpuBackend:
+    """The B200 engine behind the sharded flow: pool slots hold ciphertext rows."""
+
+    def __init__(self, ctx, keys, device):
+        self.ctx, self.keys, self.device = ctx, keys, device
+        self.row_words = ctx.params.n + 1
+
+    def reserve(self, slots):
+        self.ctx.pool_reserve(slots)
+
+    def load(self, b, lay, seed):
+        from .workloads import load_batch
+        load_batch(self.ctx, self.keys, b, lay, seed)
+
+    def program(self, ops):
+        return self.ctx.program(ops)
+
+    def export(self, first, count):
+        import torch
+        t = torch.empty((count, self.row_words), dtype=torch.int32, device=self.device)
+        if count:
+            self.ctx.store_device(first, count, t.data_ptr())
+        return t
+
+    def import_(self, first, t):
+        if t.shape[0]:
+            self.ctx.load_device(first, t.shape[0], t.data_ptr())
+
+    def read_values(self, first, Q, m):
+        bits = self.keys.decrypt_bits(self.ctx.d2h(first, Q * m)).reshape(Q, m).astype(np.uint64)
+        return (bits << np.arange(m, dtype=np.uint64)).sum(axis=1)
+
+
+class ShardedLocPir:
+    """One LocPIR batch spread over `world` ranks.  mode "boxes": every rank evaluates all
+    queries against its box shard (xor_tree mode 2), rank 0 all-gathers the partial roots
+    and runs the combine level (workloads.combine_ops).  mode "queries": every rank
+    evaluates its query shard against all boxes; outputs are gathered to rank 0.
+    Every rank holds the same seeded batch `b` (inputs are encrypted deterministically)."""
+
+    def __init__(self, backend, b, rank, world, mode, seed, folded=False):
+        from . import workloads as W
+        self.be, self.b, self.rank, self.world, self.mode = backend, b, rank, world, mode
+        Q, R, m = b.Q, b.R, b.m
+        self.prog = self.combine = None
+        if mode == "boxes":
+            self.spans = [shard_range(R, r, world) for r in range(world)]
+            self.G = sum(1 for lo, hi in self.spans if hi > lo)
+            lo, hi = self.spans[rank]
+            self.sub = W.sub_batch(b, 0, Q, lo, hi) if hi > lo else None
+            tree = 2 if world > 1 else 1
+        elif mode == "queries":
+            self.spans = [shard_range(Q, r, world) for r in range(world)]
+            lo, hi = self.spans[rank]
+            self.sub = W.sub_batch(b, lo, hi, 0, R) if hi > lo else None
+            tree = 1
+        else:
+            raise ValueError("mode must be 'boxes' or 'queries'")
+        total = 0
+        if self.sub is not None:
+            self.lay = W.PoolLayout(self.sub)
+            total = self.lay.total
+        # rank-0 regions: gathered partials / outputs, final outputs, combine scratch
+        self.part_first = total
+        parts = (self.G * Q * m) if mode == "boxes" else (Q * m)
+        self.out_first = self.part_first + parts
+        self.comb_first = self.out_first + Q * m
+        total = self.comb_first + (Q * m * (self.G + 1) if mode == "boxes" else 0)
+        backend.reserve(total)
+        if self.sub is not None:
+            backend.load(self.sub, self.lay, seed)
+            self.prog = backend.program(W.program_ops(self.sub, self.lay, tree, folded))
+        if rank == 0 and mode == "boxes" and world > 1:
+            self.combine = backend.program(W.combine_ops(self.G, Q, m, self.part_first,
+                                                         self.out_first, self.comb_first))
+
+    def local_rows(self):
+        return self.sub.Q * self.sub.m if self.sub is not None else 0
+
+    def launch(self):
+        """Local program, then the exchange (all-gather / gather to rank 0) and, for box
+        shards, rank 0's combine level."""
+        import torch.distributed as dist
+        if self.prog is not None:
+            self.prog.launch()
+        if self.world == 1:
+            return
+        b = self.b
+        out0 = int(self.lay.out.min()) if self.sub is not None else 0
+        if self.mode == "boxes":
+            t = self.be.export(out0, self.local_rows()) if self.sub is not None else \
+                self.be.export(0, 0).new_zeros((b.Q * b.m, self.be.row_words))
+            parts = [t.new_empty(t.shape) for _ in range(self.world)]
+            dist.all_gather(parts, t)
+            if self.rank == 0:
+                g = 0
+                for r, (lo, hi) in enumerate(self.spans):
+                    if hi > lo:
+                        self.be.import_(self.part_first + g * b.Q * b.m, parts[r])
+                        g += 1
+                self.combine.launch()
+        else:
+            t = self.be.export(out0, self.local_rows())
+            counts = [(hi - lo) * b.m for lo, hi in self.spans]
+            full = gather_counts_to_root(t, counts, self.rank, self.world)
+            if self.rank == 0:
+                self.be.import_(self.part_first, full)
+
+    def results(self):
+        """Rank 0: the XOR-sum value of every query of the batch; None elsewhere."""
+        if self.rank != 0:
+            return None
+        b = self.b
+        if self.world == 1:
+            return self.be.read_values(int(self.lay.out.min()), b.Q, b.m)
+        first = self.out_first if self.mode == "boxes" else self.part_first
+        return self.be.read_values(first, b.Q, b.m)
+
+    def close(self):
+        for p in (self.prog, self.combine):
+            if p is not None:
+                p.close()

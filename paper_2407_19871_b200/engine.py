@@ -264,7 +264,7 @@ class Context:
         arrs = [np.ascontiguousarray(v, np.uint32).reshape(-1)
                 for v in (x_slots, y_slots, bnd_slots, svc_slots, out_slots)]
         self._c(lib().locpir_b200_loc_pir(self.h, Q, R, l, m, *[_u32(v) for v in arrs],
-                                          scratch_first, int(bool(xor_tree))))
+                                          scratch_first, _tree_mode(xor_tree)))
 
     def debug_blind_rotate(self, lwe_n: np.ndarray) -> np.ndarray:
         """Blind rotation + extraction of combined n-dim LWEs -> N-dim LWEs (pre-KS)."""
@@ -327,6 +327,14 @@ def plan(ops) -> dict:
     return {"levels": lv.value, "blind_rotations": br.value, "key_switches": ks.value}
 
 
+def _tree_mode(xor_tree) -> int:
+    """False/0: reference chain, True/1: tree, 2: box-sharded partial (no XOR with Enc(0))."""
+    m = int(xor_tree)
+    if m not in (0, 1, 2):
+        raise ValueError("xor_tree must be 0, 1 or 2")
+    return m
+
+
 def loc_pir_program(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
                     scratch_first, xor_tree=True):
     """Host-only emission of the loc_pir gate program."""
@@ -334,10 +342,10 @@ def loc_pir_program(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slot
             for v in (x_slots, y_slots, bnd_slots, svc_slots, out_slots)]
     cnt = C.c_uint64(0)
     _check(lib().locpir_b200_loc_pir_program(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first,
-                                             int(bool(xor_tree)), None, C.byref(cnt)))
+                                             _tree_mode(xor_tree), None, C.byref(cnt)))
     ops = (GateOp * cnt.value)()
     _check(lib().locpir_b200_loc_pir_program(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first,
-                                             int(bool(xor_tree)), ops, C.byref(cnt)))
+                                             _tree_mode(xor_tree), ops, C.byref(cnt)))
     return ops
 
 
@@ -354,7 +362,7 @@ def loc_pir_folded_program(Q, R, l, m, x_slots, y_slots, boxes_signed, svc_slots
     bxp = bx.ctypes.data_as(C.POINTER(C.c_int64))
     cnt = C.c_uint64(0)
     args = (Q, R, l, m, _u32(arrs[0]), _u32(arrs[1]), bxp, _u32(arrs[2]), _u32(arrs[3]),
-            scratch_first, int(bool(xor_tree)))
+            scratch_first, _tree_mode(xor_tree))
     _check(lib().locpir_b200_loc_pir_folded_program(*args, None, C.byref(cnt)))
     ops = (GateOp * cnt.value)()
     _check(lib().locpir_b200_loc_pir_folded_program(*args, ops, C.byref(cnt)))

@@ -135,3 +135,37 @@ def read_results(ctx, keys, b: LocPirBatch, lay: PoolLayout) -> np.ndarray:
     cts = ctx.d2h(int(lay.out.min()), b.Q * b.m)
     bits = keys.decrypt_bits(cts).reshape(b.Q, b.m).astype(np.uint64)
     return (bits << np.arange(b.m, dtype=np.uint64)).sum(axis=1)
+
+
+def sub_batch(b: LocPirBatch, q_lo: int, q_hi: int, r_lo: int, r_hi: int) -> LocPirBatch:
+    """Queries [q_lo, q_hi) against boxes [r_lo, r_hi) of a batch (multi-GPU shards)."""
+    return LocPirBatch(q_hi - q_lo, r_hi - r_lo, b.l, b.m, b.x[q_lo:q_hi].copy(),
+                       b.y[q_lo:q_hi].copy(), b.boxes[r_lo:r_hi].copy(),
+                       b.payload[r_lo:r_hi].copy(), b.encrypted_bounds)
+
+
+def combine_ops(G: int, Q: int, m: int, part_first: int, out_first: int, scratch_first: int):
+    """Rank-0 combine of G box-shard partials: per query and bit
+    column a balanced XOR tree over the G partial roots, then one XOR with Enc(0) -- G
+    XOR units, so with the shards' N_g - 1 each the total stays N*m.
+    Partial (g, q, j) sits at slot part_first + (g*Q + q)*m + j; output (q, j) at
+    out_first + q*m + j.  Uses at most Q*m*G scratch slots from scratch_first."""
+    ops = []
+    nxt = scratch_first
+    for q in range(Q):
+        for j in range(m):
+            zero = nxt
+            nxt += 1
+            ops.append((_abi.CONST, 0, _abi.SLOT_NONE, _abi.SLOT_NONE, zero))
+            lvl = [part_first + (g * Q + q) * m + j for g in range(G)]
+            while len(lvl) > 1:
+                nl = []
+                for i in range(0, len(lvl) - 1, 2):
+                    ops.append((_abi.XOR, lvl[i], lvl[i + 1], _abi.SLOT_NONE, nxt))
+                    nl.append(nxt)
+                    nxt += 1
+                if len(lvl) & 1:
+                    nl.append(lvl[-1])
+                lvl = nl
+            ops.append((_abi.XOR, zero, lvl[0], _abi.SLOT_NONE, out_first + q * m + j))
+    return ops

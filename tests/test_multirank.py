@@ -69,3 +69,51 @@ def test_two_rank_gloo_sharded_gates(tmp_path):
     got = np.load(tmp_path / "got.npy")
     assert list(got) == [1, 0, 1, 1, 0]  # NAND
     assert float(np.load(tmp_path / "t.npy")[0]) == 2.0  # max over ranks
+
+
+def _sharded_worker(rank, world, port, outdir, mode, Q, R, l, m):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from plain_backend import PlainBackend
+    from paper_2407_19871_b200 import workloads as W
+    from paper_2407_19871_b200.dist import ShardedLocPir
+    b = W.make_batch(Q, R, l, m, seed=123)  # same seeded batch on every rank
+    for q in range(min(Q, R)):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    be = PlainBackend()
+    run = ShardedLocPir(be, b, rank, world, mode, seed=5)
+    run.launch()
+    got = run.results()
+    # XOR units of this rank's programs: the ranks' sum must equal the reference N*m
+    xors = 0
+    for p in (run.prog, run.combine):
+        if p is not None:
+            xors += sum(1 for op in p.ops if (op.kind if not isinstance(op, tuple) else op[0]) == 2)
+    import torch
+    t = torch.tensor([xors], dtype=torch.int64)
+    dist.all_reduce(t)
+    if rank == 0:
+        np.save(os.path.join(outdir, "got.npy"), got)
+        np.save(os.path.join(outdir, "truth.npy"), b.truth())
+        np.save(os.path.join(outdir, "xors.npy"), np.array([int(t.item())]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode,world,Q,R", [("boxes", 2, 3, 9), ("boxes", 3, 2, 2),
+                                            ("queries", 2, 5, 4), ("queries", 3, 2, 3)])
+def test_sharded_locpir_gloo(tmp_path, mode, world, Q, R):
+    """box-sharded (cfg3: partial roots all-gathered, rank-0 combine level)
+    and query-sharded (cfg4/cfg5: outputs gathered to rank 0) LocPIR over gloo, incl. a
+    rank with an empty shard; results == plaintext truth and total XOR units == N*m."""
+    l, m = 8, 3
+    mp.start_processes(_sharded_worker, args=(world, _free_port(), str(tmp_path), mode, Q, R, l, m),
+                       nprocs=world, join=True, start_method="spawn")
+    got = np.load(tmp_path / "got.npy")
+    assert np.array_equal(got, np.load(tmp_path / "truth.npy"))
+    assert int(np.load(tmp_path / "xors.npy")[0]) == Q * R * m
