@@ -195,6 +195,36 @@ int locpir_b200_debug_blind_rotate(locpir_b200_ctx* ctx, const uint32_t* lwe_n, 
 int locpir_b200_debug_keyswitch(locpir_b200_ctx* ctx, const uint32_t* lwe_N, uint64_t count,
                                 uint32_t* out_n);
 
+/* ---- wire payloads <-> device pool --------------------------------
+ * The reference's session payloads go to and from the pool without a host-side
+ * per-sample pass: one 1-D copy of the bytes plus an unpack/pack kernel.
+ *   QUERY    (protocol.hpp:185-193): two framed words, each u8 length l then l raw
+ *            samples (codec.hpp:172-193) -- the prefix leaves the second word
+ *            misaligned, so the kernel assembles words from bytes.
+ *   ZEROSHEET (circuits.hpp:46-54, :83-104): regions*bits raw zero samples; loading it
+ *            also applies preprocess_services (circuits.hpp:118-146): sample + trivial
+ *            encode_bit(service bit), region-major, bit-minor.
+ *   RESPONSE (protocol.hpp:212-227): m raw samples per query.
+ * Validation mirrors the reference's DecodeError / out_of_range checks (EINVAL with the
+ * reference's message). */
+/* Host-only framing check of one QUERY payload (no GPU needed); err may be NULL. */
+int locpir_b200_check_query_payload(const locpir_b200_params* p, const uint8_t* payload,
+                                    uint64_t len, uint32_t l, char* err, uint64_t err_len);
+/* count QUERY payloads concatenated; payload q = bytes [offsets[q], offsets[q+1]).
+ * Word bits i go to slots x_first[q] + i and y_first[q] + i (LSB first). */
+int locpir_b200_pool_load_queries(locpir_b200_ctx* c, const uint8_t* payloads,
+                                  const uint64_t* offsets, uint64_t count, uint32_t l,
+                                  const uint32_t* x_first, const uint32_t* y_first);
+/* One ZEROSHEET payload + the server's service values -> encrypted service bits at
+ * slots svc_first + r*bits + j. */
+int locpir_b200_pool_load_zero_sheet(locpir_b200_ctx* c, const uint8_t* payload, uint64_t len,
+                                     uint32_t regions, uint32_t bits,
+                                     const uint64_t* service_values, uint32_t svc_first);
+/* RESPONSE payloads of count queries (m samples from slot out_first[q] on), written
+ * back to back into payloads (count * m * 4(n+1) bytes). */
+int locpir_b200_pool_store_responses(locpir_b200_ctx* c, const uint32_t* out_first,
+                                     uint64_t count, uint32_t m, uint8_t* payloads);
+
 /* ---- flagged mode: plaintext-boundary constant folding -------------
  * The server's box boundaries are plaintext (dataset.hpp:250-253).  Comparing an
  * encrypted word against a known word folds every XNOR into a free (or no) negation and

@@ -184,6 +184,45 @@ static int golden()
         put_words("city_queries_grid_xy_int32", queries);
         put_words("city_expected", expected);
     }
+    // wire payloads: QUERY = two framed words (codec.hpp:172-193,
+    // protocol.hpp:185-193), ZEROSHEET = N*m raw zero samples (circuits.hpp:46-54, :83-89),
+    // services preprocessed with the sheet (circuits.hpp:118-146), RESPONSE = m raw samples
+    // (protocol.hpp:212-227).  Digests: FNV-1a 64 over the bytes, as (lo, hi) u32.
+    {
+        auto fnv = [](const std::vector<uint8_t>& b) {
+            uint64_t h = 1469598103934665603ull;
+            for (uint8_t c : b) {
+                h ^= c;
+                h *= 1099511628211ull;
+            }
+            return std::vector<uint32_t>{(uint32_t)h, (uint32_t)(h >> 32)};
+        };
+        const TlweParams p = TlweParams::sec128();
+        SecretKey sk = keygen(p, 12);
+        const FixedPointFormat fmt{9, 7};
+        NoiseSampler s(17, p.sigma);
+        const GeoCoordinate where(37.5665, 126.978);
+        auto q = query_payload(where, fmt, sk, s);
+        put_words("wire_query_len_lat_lon_grid",
+                  {(uint32_t)q.size(), (uint32_t)(int32_t)scale_to_grid(where.lat, fmt),
+                   (uint32_t)(int32_t)scale_to_grid(where.lon, fmt)});
+        put_words("wire_query_fnv1a64", fnv(q));
+        NoiseSampler s2(18, p.sigma);
+        auto zs = zero_sheet_payload(sk, 3, 4, s2);
+        put_words("wire_zerosheet_len", {(uint32_t)zs.size()});
+        put_words("wire_zerosheet_fnv1a64", fnv(zs));
+        auto sheet = ZeroSampleSheet::from_payload(zs, p, 3, 4);
+        auto svc = preprocess_services({5, 9, 14}, sheet, 4);
+        ByteWriter w;
+        for (const auto& sc : svc)
+            for (const auto& bit : sc.bits)
+                write_sample(w, bit.sample());
+        auto pre = w.take();
+        put_words("wire_services_5_9_14_fnv1a64", fnv(pre));
+        std::vector<uint8_t> resp(pre.begin() + 4 * sample_byte_size(p),
+                                  pre.begin() + 8 * sample_byte_size(p));
+        put_words("wire_response_region1_value", {(uint32_t)decrypt_response(resp, sk, 4)});
+    }
     // sizes (acceptance.cpp:38-101)
     {
         put_words("sample_bytes_sec80_sec128",

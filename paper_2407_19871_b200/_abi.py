@@ -78,6 +78,14 @@ SIGNATURES = [
     ("locpir_b200_loc_pir_folded_program", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.POINTER(C.c_int64), _u32p,
       _u32p, C.c_uint64, C.c_int, _ops, _u64p]),
+    ("locpir_b200_check_query_payload", C.c_int,
+     [_P, C.c_void_p, C.c_uint64, C.c_uint32, C.c_char_p, C.c_uint64]),
+    ("locpir_b200_pool_load_queries", C.c_int,
+     [_ctx, C.c_void_p, _u64p, C.c_uint64, C.c_uint32, _u32p, _u32p]),
+    ("locpir_b200_pool_load_zero_sheet", C.c_int,
+     [_ctx, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, _u64p, C.c_uint32]),
+    ("locpir_b200_pool_store_responses", C.c_int,
+     [_ctx, _u32p, C.c_uint64, C.c_uint32, C.c_void_p]),
     ("locpir_b200_debug_blind_rotate", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_debug_keyswitch", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_timing_enable", C.c_int, [_ctx, C.c_int]),

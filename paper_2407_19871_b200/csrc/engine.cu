@@ -440,6 +440,31 @@ void pool_copy(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_
     }
 }
 
+// QUERY framing check in the order the reference's ByteReader consumes the bytes
+// (handle_query, protocol.hpp:401-407: read_word x2 + expect_done; codec.hpp:180-193;
+// bytes.hpp:66-130), throwing the reference's DecodeError messages as invalid_argument.
+void check_query(uint32_t n, const uint8_t* b, uint64_t len, uint32_t l)
+{
+    const uint64_t S = 4ull * (n + 1);
+    uint64_t pos = 0;
+    for (int w = 0; w < 2; w++) {
+        if (len - pos < 1)
+            throw std::invalid_argument("truncated input: need 1 bytes, have " +
+                                        std::to_string(len - pos));
+        const uint32_t lw = b[pos++];
+        if (lw != l)
+            throw std::invalid_argument("cipher word length " + std::to_string(lw) +
+                                        " does not match negotiated format l=" +
+                                        std::to_string(l));
+        if (len - pos < (uint64_t)l * S)
+            throw std::invalid_argument("truncated input: need 4 bytes, have " +
+                                        std::to_string((len - pos) % 4));
+        pos += (uint64_t)l * S;
+    }
+    if (pos != len)
+        throw std::invalid_argument("trailing bytes: " + std::to_string(len - pos));
+}
+
 }  // namespace
 
 extern "C" {
@@ -908,6 +933,119 @@ int locpir_b200_loc_pir(locpir_b200_ctx* c, uint32_t Q, uint32_t R, uint32_t l, 
                      scratch_first, xor_tree);
         CK(cudaSetDevice(c->device));
         execute(c, v.data(), v.size());
+    });
+}
+
+int locpir_b200_check_query_payload(const locpir_b200_params* p, const uint8_t* payload,
+                                    uint64_t len, uint32_t l, char* err, uint64_t err_len)
+{
+    try {
+        if (!p || (len && !payload) || l < 2 || l > 255)
+            throw std::invalid_argument("bad arguments");
+        check_query(p->n, payload, len, l);
+        return LOCPIR_B200_OK;
+    } catch (const std::exception& e) {
+        if (err && err_len) {
+            std::snprintf(err, err_len, "%s", e.what());
+        }
+        return LOCPIR_B200_EINVAL;
+    }
+}
+
+int locpir_b200_pool_load_queries(locpir_b200_ctx* c, const uint8_t* payloads,
+                                  const uint64_t* offsets, uint64_t count, uint32_t l,
+                                  const uint32_t* x_first, const uint32_t* y_first)
+{
+    return guarded(c, [&] {
+        if (!count)
+            return;
+        if (!payloads || !offsets || !x_first || !y_first || l < 2 || l > 255)
+            throw std::invalid_argument("pool_load_queries: bad arguments");
+        for (uint64_t q = 0; q < count; q++) {
+            if (offsets[q + 1] < offsets[q])
+                throw std::invalid_argument("pool_load_queries: offsets not ascending");
+            check_query(c->p.n, payloads + offsets[q], offsets[q + 1] - offsets[q], l);
+            check_pool(c, x_first[q], l);
+            check_pool(c, y_first[q], l);
+        }
+        CK(cudaSetDevice(c->device));
+        const uint64_t base = offsets[0], bytes = offsets[count] - base;
+        c->h2d_stage.reserve((bytes + 3) / 4, c->stream, false);
+        std::vector<uint64_t> offs(offsets, offsets + count + 1);
+        for (auto& o : offs)
+            o -= base;
+        DevBuf<uint64_t> d_off;
+        DevBuf<uint32_t> d_slots;
+        d_off.reserve(count + 1, c->stream, false);
+        d_slots.reserve(2 * count, c->stream, false);
+        std::vector<uint32_t> slots(x_first, x_first + count);
+        slots.insert(slots.end(), y_first, y_first + count);
+        CK(cudaMemcpyAsync(c->h2d_stage.p, payloads + base, bytes, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d_off.p, offs.data(), (count + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d_slots.p, slots.data(), 2 * count * 4, cudaMemcpyHostToDevice, c->stream));
+        k_unpack_queries<<<c->num_sms * 4, 256, 0, c->stream>>>(
+            c->dp, reinterpret_cast<const uint8_t*>(c->h2d_stage.p), d_off.p, d_slots.p,
+            d_slots.p + count, count, l, c->pool_n.p);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));  // host vectors and temporaries go out of scope
+    });
+}
+
+int locpir_b200_pool_load_zero_sheet(locpir_b200_ctx* c, const uint8_t* payload, uint64_t len,
+                                     uint32_t regions, uint32_t bits,
+                                     const uint64_t* service_values, uint32_t svc_first)
+{
+    return guarded(c, [&] {
+        const uint64_t S = 4ull * (c->p.n + 1);
+        const uint64_t want = (uint64_t)regions * bits * S;
+        if (len != want)  // ZeroSampleSheet::from_payload (circuits.hpp:91-100)
+            throw std::invalid_argument("zero-sample sheet payload is " + std::to_string(len) +
+                                        " bytes, expected " + std::to_string(want));
+        if (!regions || !bits)
+            return;
+        if (!payload || !service_values)
+            throw std::invalid_argument("pool_load_zero_sheet: bad arguments");
+        if (bits >= 64)  // preprocess_services (circuits.hpp:125-126)
+            throw std::invalid_argument("service bit-length out of range");
+        for (uint32_t r = 0; r < regions; r++)
+            if (service_values[r] >> bits)
+                throw std::invalid_argument("service value " + std::to_string(service_values[r]) +
+                                            " does not fit in " + std::to_string(bits) + " bits");
+        check_pool(c, svc_first, (uint64_t)regions * bits);
+        CK(cudaSetDevice(c->device));
+        c->h2d_stage.reserve(len / 4, c->stream, false);
+        DevBuf<uint64_t> d_val;
+        d_val.reserve(regions, c->stream, false);
+        CK(cudaMemcpyAsync(c->h2d_stage.p, payload, len, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d_val.p, service_values, regions * 8ull, cudaMemcpyHostToDevice, c->stream));
+        k_load_zero_sheet<<<c->num_sms * 4, 256, 0, c->stream>>>(c->dp, c->h2d_stage.p, d_val.p, bits,
+                                                               regions, svc_first, c->pool_n.p);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int locpir_b200_pool_store_responses(locpir_b200_ctx* c, const uint32_t* out_first,
+                                     uint64_t count, uint32_t m, uint8_t* payloads)
+{
+    return guarded(c, [&] {
+        if (!count || !m)
+            return;
+        if (!out_first || !payloads)
+            throw std::invalid_argument("pool_store_responses: bad arguments");
+        for (uint64_t q = 0; q < count; q++)
+            check_pool(c, out_first[q], m);
+        CK(cudaSetDevice(c->device));
+        const uint64_t words = count * m * (uint64_t)(c->p.n + 1);
+        c->d2h_stage.reserve(words, c->stream, false);
+        DevBuf<uint32_t> d_first;
+        d_first.reserve(count, c->stream, false);
+        CK(cudaMemcpyAsync(d_first.p, out_first, count * 4, cudaMemcpyHostToDevice, c->stream));
+        k_pack_responses<<<c->num_sms * 4, 256, 0, c->stream>>>(c->dp, c->pool_n.p, d_first.p, count,
+                                                              m, c->d2h_stage.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(payloads, c->d2h_stage.p, words * 4, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -589,6 +589,64 @@ __global__ void k_pack_rows(DevParams dp, const uint32_t* __restrict__ pool_rows
     }
 }
 
+// Wire payloads.  QUERY: [u8 l][l samples][u8 l][l samples]; samples are
+// n+1 little-endian u32 (mask then body, torus.hpp:226-237), unaligned after the prefix.
+__global__ void k_unpack_queries(DevParams dp, const uint8_t* __restrict__ bytes,
+                                 const uint64_t* __restrict__ offs,
+                                 const uint32_t* __restrict__ xf, const uint32_t* __restrict__ yf,
+                                 uint64_t count, uint32_t l, uint32_t* __restrict__ pool_n)
+{
+    const uint32_t words = dp.n + 1;
+    const uint64_t S = 4ull * words, per_q = 2ull * l * words;
+    const uint64_t total = count * per_q;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t q = e / per_q, r = e - q * per_q;
+        const uint32_t wsel = (uint32_t)(r / ((uint64_t)l * words));
+        const uint64_t r2 = r - (uint64_t)wsel * l * words;
+        const uint32_t i = (uint32_t)(r2 / words), k = (uint32_t)(r2 - (uint64_t)i * words);
+        const uint8_t* src = bytes + offs[q] + wsel * (1 + l * S) + 1 + i * S + 4ull * k;
+        const uint32_t v = (uint32_t)src[0] | ((uint32_t)src[1] << 8) | ((uint32_t)src[2] << 16) |
+                           ((uint32_t)src[3] << 24);
+        const uint32_t slot = (wsel ? yf[q] : xf[q]) + i;
+        pool_n[(size_t)slot * dp.n_stride + k] = v;
+    }
+}
+
+// ZEROSHEET rows (aligned, packed) + preprocess_services: body += encode_bit(bit).
+__global__ void k_load_zero_sheet(DevParams dp, const uint32_t* __restrict__ sheet,
+                                  const uint64_t* __restrict__ values, uint32_t bits,
+                                  uint64_t regions, uint32_t first, uint32_t* __restrict__ pool_n)
+{
+    const uint32_t words = dp.n + 1;
+    const uint64_t total = regions * bits * words;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = e / words, k = e - g * words;
+        uint32_t v = sheet[e];
+        if (k == dp.n) {
+            const uint64_t r = g / bits, j = g - r * bits;
+            v += ((values[r] >> j) & 1) ? 0x20000000u : 0xE0000000u;
+        }
+        pool_n[(first + g) * dp.n_stride + k] = v;
+    }
+}
+
+// RESPONSE rows of several queries -> packed samples for one device-to-host copy.
+__global__ void k_pack_responses(DevParams dp, const uint32_t* __restrict__ pool_n,
+                                 const uint32_t* __restrict__ out_first, uint64_t count,
+                                 uint32_t m, uint32_t* __restrict__ packed)
+{
+    const uint32_t words = dp.n + 1;
+    const uint64_t total = count * m * words;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = e / words, k = e - g * words;
+        const uint64_t q = g / m, j = g - q * m;
+        packed[e] = pool_n[((size_t)out_first[q] + j) * dp.n_stride + k];
+    }
+}
+
 // FP64 FMA throughput probe (roofline denominator).
 __global__ void k_fp64_peak(double* out, int iters)
 {

@@ -266,6 +266,38 @@ class Context:
         self._c(lib().locpir_b200_loc_pir(self.h, Q, R, l, m, *[_u32(v) for v in arrs],
                                           scratch_first, _tree_mode(xor_tree)))
 
+    # -- wire payloads -------------------------------------
+    def load_queries(self, payloads, l: int, x_first, y_first):
+        """QUERY payloads (protocol.hpp:185-193) -> pool: word bits i at x_first[q] + i and
+        y_first[q] + i.  One 1-D copy of all payloads + an unpack kernel."""
+        buf = b"".join(payloads)
+        offs = np.zeros(len(payloads) + 1, np.uint64)
+        offs[1:] = np.cumsum([len(p) for p in payloads])
+        xf = np.ascontiguousarray(x_first, np.uint32)
+        yf = np.ascontiguousarray(y_first, np.uint32)
+        raw = np.frombuffer(buf, np.uint8) if buf else np.zeros(1, np.uint8)
+        self._c(lib().locpir_b200_pool_load_queries(
+            self.h, raw.ctypes.data, offs.ctypes.data_as(C.POINTER(C.c_uint64)), len(payloads),
+            l, _u32(xf), _u32(yf)))
+
+    def load_zero_sheet(self, payload: bytes, regions: int, bits: int, service_values, first: int):
+        """ZEROSHEET payload + service values -> encrypted service bits (preprocess_services,
+        circuits.hpp:118-146) at slots first + r*bits + j."""
+        vals = np.ascontiguousarray(service_values, np.uint64)
+        raw = np.frombuffer(payload, np.uint8) if payload else np.zeros(1, np.uint8)
+        self._c(lib().locpir_b200_pool_load_zero_sheet(
+            self.h, raw.ctypes.data, len(payload), regions, bits,
+            vals.ctypes.data_as(C.POINTER(C.c_uint64)), first))
+
+    def store_responses(self, out_first, m: int) -> list:
+        """RESPONSE payloads (protocol.hpp:212-227), one bytes object per query."""
+        of = np.ascontiguousarray(out_first, np.uint32)
+        S = 4 * (self.params.n + 1)
+        out = np.zeros(max(1, len(of) * m * S), np.uint8)
+        self._c(lib().locpir_b200_pool_store_responses(self.h, _u32(of), len(of), m,
+                                                       out.ctypes.data))
+        return [out[q * m * S:(q + 1) * m * S].tobytes() for q in range(len(of))]
+
     def debug_blind_rotate(self, lwe_n: np.ndarray) -> np.ndarray:
         """Blind rotation + extraction of combined n-dim LWEs -> N-dim LWEs (pre-KS)."""
         lwe_n = np.ascontiguousarray(lwe_n, np.uint32).reshape(-1, self.params.n + 1)
@@ -325,6 +357,17 @@ def plan(ops) -> dict:
     ks = C.c_uint64()
     _check(lib().locpir_b200_plan(arr, len(ops), C.byref(lv), C.byref(br), C.byref(ks)))
     return {"levels": lv.value, "blind_rotations": br.value, "key_switches": ks.value}
+
+
+def check_query_payload(params: "TfheParams", payload: bytes, l: int):
+    """Host-only QUERY framing check; raises InvalidArgument with the reference's
+    DecodeError message (codec.hpp:180-193, bytes.hpp:118-130)."""
+    err = C.create_string_buffer(256)
+    raw = np.frombuffer(payload, np.uint8) if payload else np.zeros(1, np.uint8)
+    rc = lib().locpir_b200_check_query_payload(C.byref(params.c), raw.ctypes.data, len(payload),
+                                               l, err, 256)
+    if rc:
+        raise InvalidArgument(err.value.decode())
 
 
 def _tree_mode(xor_tree) -> int:
