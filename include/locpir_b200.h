@@ -225,6 +225,30 @@ int locpir_b200_pool_load_zero_sheet(locpir_b200_ctx* c, const uint8_t* payload,
 int locpir_b200_pool_store_responses(locpir_b200_ctx* c, const uint32_t* out_first,
                                      uint64_t count, uint32_t m, uint8_t* payloads);
 
+/* ---- cross-session query batcher -----------------------------------
+ * Server::handle_zerosheet / handle_query (protocol.hpp:373-424) without the transport:
+ * sessions register their ZEROSHEET once, QUERY payloads from any session queue up, and
+ * flush() answers all of them with ONE level-scheduled program (each query reads its own
+ * session's preprocessed services), producing RESPONSE payloads per ticket.  boxes: [R][4]
+ * signed l-bit grid values (x1, x2, y1, y2) of the server's dataset; services: [R] values.
+ * folded = 1 uses the plaintext-boundary constant-folded circuit (flagged mode). */
+typedef struct locpir_b200_server locpir_b200_server;
+int locpir_b200_server_create(locpir_b200_ctx* c, const int64_t* boxes, const uint64_t* services,
+                              uint32_t R, uint32_t l, uint32_t m, uint32_t max_sessions,
+                              int folded, locpir_b200_server** out);
+void locpir_b200_server_destroy(locpir_b200_server* s);
+const char* locpir_b200_server_last_error(const locpir_b200_server* s);
+int locpir_b200_server_open_session(locpir_b200_server* s, const uint8_t* zero_sheet, uint64_t len,
+                                    uint32_t* session);
+int locpir_b200_server_close_session(locpir_b200_server* s, uint32_t session);
+int locpir_b200_server_submit(locpir_b200_server* s, uint32_t session, const uint8_t* query,
+                              uint64_t len, uint64_t* ticket);
+uint64_t locpir_b200_server_pending(const locpir_b200_server* s);
+int locpir_b200_server_flush(locpir_b200_server* s, uint64_t* answered);
+/* RESPONSE payload of a flushed ticket (m * 4(n+1) bytes); ELOGIC if not answered yet. */
+int locpir_b200_server_take_response(locpir_b200_server* s, uint64_t ticket, uint8_t* out,
+                                     uint64_t len);
+
 /* ---- flagged mode: plaintext-boundary constant folding -------------
  * The server's box boundaries are plaintext (dataset.hpp:250-253).  Comparing an
  * encrypted word against a known word folds every XNOR into a free (or no) negation and

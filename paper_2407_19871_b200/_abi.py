@@ -86,6 +86,19 @@ SIGNATURES = [
      [_ctx, C.c_void_p, C.c_uint64, C.c_uint32, C.c_uint32, _u64p, C.c_uint32]),
     ("locpir_b200_pool_store_responses", C.c_int,
      [_ctx, _u32p, C.c_uint64, C.c_uint32, C.c_void_p]),
+    ("locpir_b200_server_create", C.c_int,
+     [_ctx, C.POINTER(C.c_int64), _u64p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+      C.POINTER(C.c_void_p)]),
+    ("locpir_b200_server_destroy", None, [C.c_void_p]),
+    ("locpir_b200_server_last_error", C.c_char_p, [C.c_void_p]),
+    ("locpir_b200_server_open_session", C.c_int,
+     [C.c_void_p, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint32)]),
+    ("locpir_b200_server_close_session", C.c_int, [C.c_void_p, C.c_uint32]),
+    ("locpir_b200_server_submit", C.c_int,
+     [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]),
+    ("locpir_b200_server_pending", C.c_uint64, [C.c_void_p]),
+    ("locpir_b200_server_flush", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    ("locpir_b200_server_take_response", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     ("locpir_b200_debug_blind_rotate", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_debug_keyswitch", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_timing_enable", C.c_int, [_ctx, C.c_int]),

@@ -81,10 +81,13 @@ inline void emit_xor_root(Emitter& e, std::vector<uint32_t> lvl, uint32_t zero, 
 // loc_pir (circuits.hpp:276-324) for Q queries.  xor_tree = 0 keeps the
 // reference's N-long chain per bit column (circuits.hpp:257-261); 1 uses a
 // balanced tree of N-1 XORs plus one XOR with Enc(0): still N*m XOR units.
-inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
-                         uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
-                         const uint32_t* bnd, const uint32_t* svc, const uint32_t* out,
-                         uint64_t scratch_first, int xor_tree)
+// svc(q, r, j) -> pool slot of service bit j of region r as seen by query q (shared
+// across queries for one session; per session in the cross-session batcher).
+template <class SvcFn>
+inline void emit_loc_pir_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
+                            uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
+                            const uint32_t* bnd, SvcFn svc, const uint32_t* out,
+                            uint64_t scratch_first, int xor_tree)
 {
     Emitter e{&ops, scratch_first};
     std::vector<uint32_t> masked((size_t)R * m);
@@ -104,7 +107,7 @@ inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint
             const uint32_t v2 = e.gate(LOCPIR_B200_AND, y_l, y_r);
             const uint32_t f = e.gate(LOCPIR_B200_AND, v1, v2);
             for (uint32_t j = 0; j < m; j++)  // mask_service (circuits.hpp:219-227)
-                masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc[(size_t)r * m + j]);
+                masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc(q, r, j));
         }
         // xor_sum_services (circuits.hpp:240-269)
         for (uint32_t j = 0; j < m; j++) {
@@ -172,10 +175,11 @@ inline uint64_t loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint3
 }
 
 // loc_pir with plaintext boxes [R][4] = (x1, x2, y1, y2): x1 <= x = NOT(x < x1).
-inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
-                                uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
-                                const int64_t* boxes, const uint32_t* svc, const uint32_t* out,
-                                uint64_t scratch_first, int xor_tree)
+template <class SvcFn>
+inline void emit_loc_pir_folded_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
+                                   uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
+                                   const int64_t* boxes, SvcFn svc, const uint32_t* out,
+                                   uint64_t scratch_first, int xor_tree)
 {
     Emitter e{&ops, scratch_first};
     std::vector<uint32_t> masked((size_t)R * m);
@@ -192,7 +196,7 @@ inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t 
             const uint32_t v2 = e.gate(LOCPIR_B200_AND, y_l, y_r);
             const uint32_t f = e.gate(LOCPIR_B200_AND, v1, v2);
             for (uint32_t j = 0; j < m; j++)
-                masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc[(size_t)r * m + j]);
+                masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc(q, r, j));
         }
         for (uint32_t j = 0; j < m; j++) {
             const uint32_t dst = out[(size_t)q * m + j];
@@ -209,6 +213,27 @@ inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t 
             emit_xor_root(e, lvl, zero, dst, xor_tree);
         }
     }
+}
+
+// Shared service table [R][m] (one session / the reference's single-session server).
+inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
+                         uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
+                         const uint32_t* bnd, const uint32_t* svc, const uint32_t* out,
+                         uint64_t scratch_first, int xor_tree)
+{
+    emit_loc_pir_fn(ops, Q, R, l, m, xs, ys, bnd,
+                    [&](uint32_t, uint32_t r, uint32_t j) { return svc[(size_t)r * m + j]; }, out,
+                    scratch_first, xor_tree);
+}
+
+inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
+                                uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
+                                const int64_t* boxes, const uint32_t* svc, const uint32_t* out,
+                                uint64_t scratch_first, int xor_tree)
+{
+    emit_loc_pir_folded_fn(ops, Q, R, l, m, xs, ys, boxes,
+                           [&](uint32_t, uint32_t r, uint32_t j) { return svc[(size_t)r * m + j]; },
+                           out, scratch_first, xor_tree);
 }
 
 }  // namespace lpb

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/locpir_b200.h"
+#include "server.hpp"
 #include "circuits.hpp"
 #include "kernels.cuh"
 #include "br_warp.cuh"
@@ -1046,6 +1047,108 @@ int locpir_b200_pool_store_responses(locpir_b200_ctx* c, const uint32_t* out_fir
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(payloads, c->d2h_stage.p, words * 4, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- cross-session batcher (server.hpp) ---------------------------------------------
+int locpir_b200_server_create(locpir_b200_ctx* c, const int64_t* boxes, const uint64_t* services,
+                              uint32_t R, uint32_t l, uint32_t m, uint32_t max_sessions,
+                              int folded, locpir_b200_server** out)
+{
+    if (!c || !boxes || !services || !out || !R || l < 2 || l > 63 || !m || m >= 64 ||
+        !max_sessions)
+        return LOCPIR_B200_EINVAL;
+    *out = nullptr;
+    auto s = std::make_unique<locpir_b200_server>();
+    s->ctx = c;
+    s->R = R;
+    s->l = l;
+    s->m = m;
+    s->n = c->p.n;
+    s->max_sessions = max_sessions;
+    s->folded = folded ? 1 : 0;
+    s->boxes.assign(boxes, boxes + (size_t)R * 4);
+    s->services.assign(services, services + R);
+    const int rc = lpb::srv_guard(s.get(), [&] {
+        for (int64_t v : s->boxes)
+            if (v < -(1ll << (l - 1)) || v >= (1ll << (l - 1)))
+                throw std::invalid_argument("box boundary does not fit in l bits");
+        for (uint64_t v : s->services)
+            if (v >> m)
+                throw std::invalid_argument("service value " + std::to_string(v) +
+                                            " does not fit in " + std::to_string(m) + " bits");
+        lpb::srv_init(s.get());
+    });
+    if (rc) {
+        c->err = s->err;
+        return rc;
+    }
+    *out = s.release();
+    return LOCPIR_B200_OK;
+}
+
+void locpir_b200_server_destroy(locpir_b200_server* s) { delete s; }
+
+const char* locpir_b200_server_last_error(const locpir_b200_server* s)
+{
+    return s ? s->err.c_str() : "";
+}
+
+int locpir_b200_server_open_session(locpir_b200_server* s, const uint8_t* zero_sheet, uint64_t len,
+                                    uint32_t* session)
+{
+    return lpb::srv_guard(s, [&] {
+        if (!session || (len && !zero_sheet))
+            throw std::invalid_argument("open_session: bad arguments");
+        *session = lpb::srv_open(s, zero_sheet, len);
+    });
+}
+
+int locpir_b200_server_close_session(locpir_b200_server* s, uint32_t session)
+{
+    return lpb::srv_guard(s, [&] {
+        if (session >= s->max_sessions || !s->open[session])
+            throw std::invalid_argument("unknown session");
+        for (const auto& p : s->pending)
+            if (p.session == session)
+                throw std::logic_error("session has queries pending; flush first");
+        s->open[session] = 0;
+    });
+}
+
+int locpir_b200_server_submit(locpir_b200_server* s, uint32_t session, const uint8_t* query,
+                              uint64_t len, uint64_t* ticket)
+{
+    return lpb::srv_guard(s, [&] {
+        if (!ticket || (len && !query))
+            throw std::invalid_argument("submit: bad arguments");
+        *ticket = lpb::srv_submit(s, session, query, len);
+    });
+}
+
+uint64_t locpir_b200_server_pending(const locpir_b200_server* s) { return s ? s->pending.size() : 0; }
+
+int locpir_b200_server_flush(locpir_b200_server* s, uint64_t* answered)
+{
+    return lpb::srv_guard(s, [&] {
+        const uint64_t n = lpb::srv_flush(s);
+        if (answered)
+            *answered = n;
+    });
+}
+
+int locpir_b200_server_take_response(locpir_b200_server* s, uint64_t ticket, uint8_t* out,
+                                     uint64_t len)
+{
+    return lpb::srv_guard(s, [&] {
+        auto it = s->responses.find(ticket);
+        if (it == s->responses.end())
+            throw std::logic_error("ticket " + std::to_string(ticket) + " has no response (not flushed)");
+        if (!out || len != it->second.size())
+            throw std::invalid_argument("response buffer must be " + std::to_string(it->second.size()) +
+                                        " bytes");
+        std::memcpy(out, it->second.data(), len);
+        s->responses.erase(it);
     });
 }
 
