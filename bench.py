@@ -376,9 +376,61 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                                                            "once the GPU is saturated)",
             }
             run.close()
+    out["cfg4_server"] = run_server_sample(ctx128, keys128, ws, max_over_ranks)
     if ctx80 is not None:
         ctx80.close()
     return out
+
+
+def run_server_sample(ctx, keys, ws, max_over_ranks, Q=256, sessions=8):
+    """cfg4's shape through the cross-session batcher: QUERY payload bytes
+    of `sessions` sessions in, RESPONSE bytes out.  The timed region holds submit (framing
+    checks), flush (one H2D of all payloads + unpack, planning, the batched program,
+    response pack + one D2H) and take_response; sessions' zero sheets are registered
+    before it.  Replicas per GPU."""
+    import torch
+    from paper_2407_19871_b200 import workloads as W
+    from paper_2407_19871_b200.server import BatchingServer
+    sec, _, R, l, m, _ = W.CONFIGS["cfg4"]
+    b = W.make_batch(Q, R, l, m, seed=KEY_SEED + 9)
+    for q in range(min(Q, R)):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    srv = BatchingServer(ctx, W.signed_boxes(b), b.payload, l, m, max_sessions=sessions)
+    n1 = ctx.params.n + 1
+    # client side (untimed): zero sheets = Enc(-1/8) + 1/8 = Enc(0); framed query words
+    sids = []
+    for s_ in range(sessions):
+        z = keys.encrypt_bits(np.zeros(R * m, np.uint8), 7000 + s_)
+        z[:, -1] += np.uint32(0x20000000)
+        sids.append(srv.open_session(z.astype("<u4").tobytes()))
+    xb = W._bits_signed(b.x, l)
+    yb = W._bits_signed(b.y, l)
+    cx = keys.encrypt_bits(xb.reshape(-1), 8000).reshape(Q, l, n1)
+    cy = keys.encrypt_bits(yb.reshape(-1), 8001).reshape(Q, l, n1)
+    payloads = [bytes([l]) + cx[q].astype("<u4").tobytes() + bytes([l]) + cy[q].astype("<u4").tobytes()
+                for q in range(Q)]
+
+    def one_round():
+        tickets = [srv.submit(sids[q % sessions], payloads[q]) for q in range(Q)]
+        srv.flush()
+        return [srv.take_response(t) for t in tickets]
+
+    one_round()  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    resp = one_round()
+    dt = max_over_ranks(time.perf_counter() - t0)
+    got = np.array([(keys.decrypt_bits(np.frombuffer(r, "<u4").reshape(m, n1)).astype(np.uint64)
+                     << np.arange(m, dtype=np.uint64)).sum() for r in resp], np.uint64)
+    srv.close()
+    return {"queries_per_s": ws * Q / dt, "ms_per_batch": dt * 1e3, "queries_per_gpu": Q,
+            "sessions": sessions, "boxes": R, "l": l, "m": m, "security_bits": sec,
+            "correct": bool(np.array_equal(got, b.truth())),
+            "h2d_bytes_per_batch": sum(len(p_) for p_ in payloads),
+            "d2h_bytes_per_batch": Q * m * 4 * n1,
+            "mode": "wire path: QUERY bytes -> batched loc_pir -> RESPONSE bytes (host clock, "
+                    "includes payload copies, framing checks and planning)"}
 
 
 # ---------------------------------------------------------------------------

@@ -163,7 +163,10 @@ class Context:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:  # interpreter shutdown may already have torn down the module globals
+            self.close()
+        except Exception:
+            pass
 
     def _c(self, rc):
         _check(rc, self.h)
@@ -346,7 +349,10 @@ class Program:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:  # interpreter shutdown may already have torn down the module globals
+            self.close()
+        except Exception:
+            pass
 
 
 def plan(ops) -> dict:

@@ -79,4 +79,7 @@ class BatchingServer:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:  # interpreter shutdown may already have torn down the module globals
+            self.close()
+        except Exception:
+            pass
