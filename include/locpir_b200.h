@@ -249,6 +249,18 @@ int locpir_b200_server_flush(locpir_b200_server* s, uint64_t* answered);
 int locpir_b200_server_take_response(locpir_b200_server* s, uint64_t ticket, uint8_t* out,
                                      uint64_t len);
 
+/* ---- client-side batched encryption on the device --------------------
+ * Encrypts torus messages mus[j] under the client's LWE key (n bytes, 0/1) into pool
+ * slots first_slot + j, with the counter-based stream of csrc/cbrng.h (Philox4x32-10 +
+ * IEEE-exact Box-Muller, noise alpha_in): sample j uses stream index first_index + j, so
+ * the output is a pure function of (key, seed, index, mu) and equals the CPU definition
+ * bit for bit.  mu = +-1/8 encrypts bits (torus.hpp:52-55, :172-175); mu = 0 makes the
+ * zero-sample sheet (circuits.hpp:46-54).  Flagged mode: not the reference's mt19937_64
+ * stream (torus.hpp:119-138). */
+int locpir_b200_client_encrypt(locpir_b200_ctx* c, const uint8_t* lwe_key, uint64_t seed,
+                               uint32_t first_index, const uint32_t* mus, uint64_t count,
+                               uint64_t first_slot);
+
 /* ---- flagged mode: plaintext-boundary constant folding -------------
  * The server's box boundaries are plaintext (dataset.hpp:250-253).  Comparing an
  * encrypted word against a known word folds every XNOR into a free (or no) negation and

@@ -92,6 +92,17 @@ def lib():
         L.or_external_product.argtypes = [C.POINTER(KeySet), C.c_uint32, u32p, C.c_int, u32p]
         L.or_keyswitch.argtypes = [C.POINTER(KeySet), u32p, u32p]
         L.or_gate.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_int, u32p]
+        L.or_cb_encrypt.argtypes = [u8p, C.c_uint32, C.c_uint64, C.c_uint32, u32p, C.c_uint64,
+                                    C.c_double, u32p]
+        L.or_cb_encrypt.restype = None
+        L.or_cb_philox.argtypes = [u32p, C.c_uint64, u32p]
+        L.or_cb_philox.restype = None
+        L.or_cb_log.argtypes = [C.c_double]
+        L.or_cb_log.restype = C.c_double
+        L.or_cb_cos2pi.argtypes = [C.c_double]
+        L.or_cb_cos2pi.restype = C.c_double
+        L.or_cb_noise.argtypes = [C.c_uint64, C.c_uint32, C.c_double]
+        L.or_cb_noise.restype = C.c_uint32
         L.or_gate_list.argtypes = [C.POINTER(KeySet), C.POINTER(GateItem), C.c_uint64, C.c_int,
                                    C.c_int]
         L.or_gate_batch.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_uint64,
@@ -337,3 +348,19 @@ def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: in
                 pool[o] = 0
                 pool[o, n] = 0x20000000 if a else 0xE0000000
     return pool
+
+
+def cb_encrypt(key: np.ndarray, seed: int, first_index: int, mus, alpha: float) -> np.ndarray:
+    """Counter-based client encryption (cbrng.h stream) of torus messages `mus`."""
+    mus = np.ascontiguousarray(mus, np.uint32).reshape(-1)
+    key = np.ascontiguousarray(key, np.uint8)
+    out = np.zeros((mus.size, key.size + 1), np.uint32)
+    lib().or_cb_encrypt(_u8(key), key.size, seed, first_index, _u32(mus), mus.size, alpha, _u32(out))
+    return out
+
+
+def cb_philox(ctr, seed: int) -> list:
+    c = np.ascontiguousarray(ctr, np.uint32)
+    o = np.zeros(4, np.uint32)
+    lib().or_cb_philox(_u32(c), seed, _u32(o))
+    return [int(v) for v in o]

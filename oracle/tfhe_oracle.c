@@ -853,3 +853,29 @@ int or_gate_list(const or_keyset* ks, const or_gate_item* items, uint64_t count,
     free(tid);
     return rc;
 }
+
+/* ---- counter-based client encryption ------------------------------
+ * The stream is DEFINED by paper_2407_19871_b200/csrc/cbrng.h (one definition for CPU and
+ * GPU); the oracle evaluates it on the host so the device kernel can be checked bit for
+ * bit.  Philox itself is pinned to its published known answers in the tests. */
+#include "../paper_2407_19871_b200/csrc/cbrng.h"
+
+void or_cb_philox(const uint32_t ctr[4], uint64_t seed, uint32_t out[4]) { cb_philox(ctr, seed, out); }
+double or_cb_log(double u) { return cb_log(u); }
+double or_cb_cos2pi(double x) { return cb_cos2pi(x); }
+uint32_t or_cb_noise(uint64_t seed, uint32_t index, double alpha) { return cb_noise(seed, index, alpha); }
+
+void or_cb_encrypt(const uint8_t* key, uint32_t n, uint64_t seed, uint32_t first_index,
+                   const uint32_t* mus, uint64_t count, double alpha, uint32_t* out)
+{
+    for (uint64_t j = 0; j < count; j++) {
+        const uint32_t idx = first_index + (uint32_t)j;
+        uint32_t* o = out + j * (n + 1);
+        uint32_t dot = 0;
+        for (uint32_t i = 0; i < n; i++) {
+            o[i] = cb_mask_word(seed, idx, i);
+            dot += o[i] * (uint32_t)key[i];
+        }
+        o[n] = dot + mus[j] + cb_noise(seed, idx, alpha);
+    }
+}

@@ -154,6 +154,16 @@ int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
 int or_gate_batch(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
                   uint32_t* out, uint64_t count, int mode, int threads);
 
+/* Counter-based client encryption (paper_2407_19871_b200/csrc/cbrng.h):
+ * sample j = (mask philox words, body = <a, key> + mus[j] + noise) with stream index
+ * first_index + j.  Also exported: the Philox block and the Gaussian pieces for pins. */
+void or_cb_encrypt(const uint8_t* key, uint32_t n, uint64_t seed, uint32_t first_index,
+                   const uint32_t* mus, uint64_t count, double alpha, uint32_t* out);
+void or_cb_philox(const uint32_t ctr[4], uint64_t seed, uint32_t out[4]);
+double or_cb_log(double u);
+double or_cb_cos2pi(double x);
+uint32_t or_cb_noise(uint64_t seed, uint32_t index, double alpha);
+
 /* Heterogeneous gate list on `threads` host threads (static block partition as
  * parallel.hpp:15-52): one level of a gate program. */
 typedef struct {

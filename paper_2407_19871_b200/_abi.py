@@ -99,6 +99,8 @@ SIGNATURES = [
     ("locpir_b200_server_pending", C.c_uint64, [C.c_void_p]),
     ("locpir_b200_server_flush", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     ("locpir_b200_server_take_response", C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    ("locpir_b200_client_encrypt", C.c_int,
+     [_ctx, _u8p, C.c_uint64, C.c_uint32, _u32p, C.c_uint64, C.c_uint64]),
     ("locpir_b200_debug_blind_rotate", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_debug_keyswitch", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_timing_enable", C.c_int, [_ctx, C.c_int]),

@@ -3,6 +3,7 @@
 // kernels.cuh; no CPU fallback exists: every gate runs on the GPU.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1149,6 +1150,37 @@ int locpir_b200_server_take_response(locpir_b200_server* s, uint64_t ticket, uin
                                         " bytes");
         std::memcpy(out, it->second.data(), len);
         s->responses.erase(it);
+    });
+}
+
+int locpir_b200_client_encrypt(locpir_b200_ctx* c, const uint8_t* lwe_key, uint64_t seed,
+                               uint32_t first_index, const uint32_t* mus, uint64_t count,
+                               uint64_t first_slot)
+{
+    return guarded(c, [&] {
+        if (!count)
+            return;
+        if (!lwe_key || !mus)
+            throw std::invalid_argument("client_encrypt: bad arguments");
+        if ((uint64_t)first_index + count > (1ull << 32))
+            throw std::invalid_argument("client_encrypt: stream index range exceeds 2^32");
+        for (uint32_t i = 0; i < c->p.n; i++)
+            if (lwe_key[i] > 1)
+                throw std::invalid_argument("client_encrypt: key bits must be 0 or 1");
+        check_pool(c, first_slot, count);
+        CK(cudaSetDevice(c->device));
+        DevBuf<uint8_t> d_key;
+        DevBuf<uint32_t> d_mu;
+        d_key.reserve(c->p.n, c->stream, false);
+        d_mu.reserve(count, c->stream, false);
+        CK(cudaMemcpyAsync(d_key.p, lwe_key, c->p.n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(d_mu.p, mus, count * 4, cudaMemcpyHostToDevice, c->stream));
+        const uint64_t blocks = std::min<uint64_t>((count + 7) / 8, (uint64_t)c->num_sms * 16);
+        k_client_encrypt<<<(unsigned)blocks, 256, 0, c->stream>>>(c->dp, d_key.p, seed, first_index,
+                                                                d_mu.p, count, c->p.alpha_in,
+                                                                first_slot, c->pool_n.p);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
     });
 }
 

@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include "fft.cuh"
+#include "cbrng.h"
 
 namespace lpb {
 
@@ -647,6 +648,43 @@ __global__ void k_pack_responses(DevParams dp, const uint32_t* __restrict__ pool
     }
 }
 
+// Counter-based client encryption (cbrng.h): one warp per sample; lanes
+// generate Philox blocks of 4 mask words, the <a, key> sum is reduced mod 2^32 across
+// the warp (order-free), lane 0 adds mu and the Box-Muller noise.
+__global__ void k_client_encrypt(DevParams dp, const uint8_t* __restrict__ key, uint64_t seed,
+                                 uint32_t first_index, const uint32_t* __restrict__ mus,
+                                 uint64_t count, double alpha, uint64_t first_slot,
+                                 uint32_t* __restrict__ pool_n)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint32_t n = dp.n, blocks = (n + 3) / 4;
+    for (uint64_t j = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < count;
+         j += warps) {
+        const uint32_t idx = first_index + (uint32_t)j;
+        uint32_t* o = pool_n + (first_slot + j) * dp.n_stride;
+        uint32_t dot = 0;
+        for (uint32_t b = lane; b < blocks; b += 32) {
+            const uint32_t ctr[4] = {idx, b, 0u, 0u};
+            uint32_t r[4];
+            cb_philox(ctr, seed, r);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const uint32_t i = 4 * b + q;
+                if (i < n) {
+                    o[i] = r[q];
+                    dot += r[q] * (uint32_t)key[i];
+                }
+            }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1)
+            dot += __shfl_xor_sync(0xFFFFFFFFu, dot, off);
+        if (lane == 0)
+            o[n] = dot + mus[j] + cb_noise(seed, idx, alpha);
+    }
+}
+
 // FP64 FMA throughput probe (roofline denominator).
 __global__ void k_fp64_peak(double* out, int iters)
 {
@@ -742,6 +780,7 @@ struct LatSmem {
     uint32_t acc[2][1024];
     double2 tws[FFT_M];
     double2 F[2 * L][FFT_M];              // digit spectra, slot layout [q*64 + t]
+    double2 O[2][FFT_M];                  // MAC results per output component
     double2 tiles[2 * L][2][XTILE];       // per group: cross-warp tile, intra-warp tile
     uint16_t abar[MAX_N + 1];
 };
@@ -801,11 +840,29 @@ __global__ void __launch_bounds__(128 * L, 1)
     const int c = g / L, p = g % L;
     const int sh = 32 - (p + 1) * BGBIT;
 
+    // MAC split over all 2L groups: group g serves output component g / L and the
+    // frequency slots q*64 + t with q = g % L + L*k (at most P of them per thread); each
+    // slot's chain over the 2L rows keeps the oracle's order, so the result is unchanged.
+    constexpr int P = (8 + L - 1) / L;
+    const int mcomp = g / L, msub = g % L;
     for (uint32_t i = 0; i < n; i++) {
         __syncthreads();
         const uint32_t a = S.abar[i];
         if (a == 0)
             continue;
+        // this thread's BK values for its MAC slots, in flight during the transform
+        double2 bkv[ROWS][P];
+        {
+            const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M + (size_t)mcomp * FFT_M;
+#pragma unroll
+            for (int r = 0; r < ROWS; r++)
+#pragma unroll
+                for (int k = 0; k < P; k++) {
+                    const int q = msub + L * k;
+                    if (q < 8)
+                        bkv[r][k] = ld_stream(bki + (size_t)r * 2 * FFT_M + q * 64 + t);
+                }
+        }
         // every group: digit (c, p) of (X^a - 1) ACC_c -> forward transform -> F[g]
         {
             double2 x[8];
@@ -824,21 +881,25 @@ __global__ void __launch_bounds__(128 * L, 1)
                 S.F[g][q * 64 + t] = x[q];
         }
         __syncthreads();
-        // groups 0 / 1: MAC chain over the rows in oracle order, inverse, ACC update
+#pragma unroll
+        for (int k = 0; k < P; k++) {
+            const int q = msub + L * k;
+            if (q < 8) {
+                double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int r = 0; r < ROWS; r++)
+                    mac(o, S.F[r][q * 64 + t], bkv[r][k]);
+                S.O[mcomp][q * 64 + t] = o;
+            }
+        }
+        __syncthreads();
+        // groups 0 / 1: inverse transform of output component g, ACC update
         if (g < 2) {
             const int comp = g;
-            const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M + (size_t)comp * FFT_M;
             double2 o[8];
 #pragma unroll
             for (int q = 0; q < 8; q++)
-                o[q] = make_double2(0.0, 0.0);
-#pragma unroll
-            for (int r = 0; r < ROWS; r++) {
-                const double2* row = bki + (size_t)r * 2 * FFT_M;
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    mac(o[q], S.F[r][q * 64 + t], ld_stream(row + q * 64 + t));
-            }
+                o[q] = S.O[comp][q * 64 + t];
             fft_inverse(o, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
 #pragma unroll
             for (int q = 0; q < 8; q++) {

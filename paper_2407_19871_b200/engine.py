@@ -301,6 +301,15 @@ class Context:
                                                        out.ctypes.data))
         return [out[q * m * S:(q + 1) * m * S].tobytes() for q in range(len(of))]
 
+    # -- client-side encryption on the device (flagged stream) -----
+    def client_encrypt(self, lwe_key, seed: int, mus, first_slot: int, first_index: int = 0):
+        """Encrypt torus messages into pool slots with the counter-based stream
+        (csrc/cbrng.h); bit b -> mu = 0x20000000 if b else 0xE0000000, zero sheet mu = 0."""
+        key = np.ascontiguousarray(lwe_key, np.uint8)
+        mus = np.ascontiguousarray(mus, np.uint32).reshape(-1)
+        self._c(lib().locpir_b200_client_encrypt(self.h, _u8(key), seed, first_index, _u32(mus),
+                                                 mus.size, first_slot))
+
     def debug_blind_rotate(self, lwe_n: np.ndarray) -> np.ndarray:
         """Blind rotation + extraction of combined n-dim LWEs -> N-dim LWEs (pre-KS)."""
         lwe_n = np.ascontiguousarray(lwe_n, np.uint32).reshape(-1, self.params.n + 1)
