@@ -53,6 +53,20 @@ def committed_traffic(kernel="k_blind_rotate<3, 7>"):
         return None
 
 
+def hbm_view(G, params, avg_br_ms):
+    """K1 against the measured HBM roof: algorithmic and ncu-measured DRAM bytes per launch
+    over the launch time (MEASURED_PEAKS.json hbm_gbs)."""
+    try:
+        peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        peak = None
+    alg = G * (2 * 4 * (params.n + 1) + 4 * (params.N + 1)) + params.bk_words() * 8
+    t = committed_traffic() if G == GATES_PER_GPU else None
+    secs = avg_br_ms * 1e-3
+    return {"algorithmic_GBps": alg / secs / 1e9, "dram_GBps": t / secs / 1e9 if t else None,
+            "peak_GBps": peak, "frac": (t or alg) / secs / 1e9 / peak if peak else None}
+
+
 def workload_config(n_gpus):
     return {
         "workload": "cfg2: 65,536 independent bootstrapped NAND gates per GPU, 128-bit TFHE "
@@ -551,6 +565,10 @@ def run_b200(args):
                 "peak_source": "measured live on this GPU: k_fp64_peak DFMA microbenchmark "
                                "(MEASURED_PEAKS.json has no FP64 figure)",
                 "step_share": br_ms / max(1e-9, br_ms + ks_ms),
+                "bound_note": "FP64 pipe: per-ciphertext negacyclic FFTs are dense FP64 work "
+                              "with no shared contraction (SURVEY §8(d)), so neither the HBM "
+                              "nor the tensor-core roof applies; hbm_view shows the HBM side",
+                "hbm_view": hbm_view(G, params, avg_br_ms),
             },
             "keyswitch": {"avg_launch_ms": avg_ks_ms,
                           "ksk_GBps_if_read_once": ksk_bytes / (avg_ks_ms * 1e-3) / 1e9},

@@ -875,7 +875,9 @@ __global__ void __launch_bounds__(128 * L, 1)
                 const int dhi = (int)((hi >> sh) & MASK) - (int)HALF;
                 x[q] = cmul(make_double2((double)dlo, (double)dhi), S.tws[j]);
             }
+#if !LAT_SKIP_FWD
             fft_forward(x, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
+#endif
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 S.F[g][q * 64 + t] = x[q];
@@ -900,7 +902,9 @@ __global__ void __launch_bounds__(128 * L, 1)
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 o[q] = S.O[comp][q * 64 + t];
+#if !LAT_SKIP_INV
             fft_inverse(o, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
+#endif
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 const int j = t + 64 * q;
