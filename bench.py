@@ -354,11 +354,15 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
             b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
             b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
         be = GpuBackend(ctx, keys, torch.device("cuda", local))
-        # folded: flagged plaintext-boundary mode, not the reference count
-        for folded in ((False, True) if not enc else (False,)):
+        # flagged modes (not the reference count): "folded" = plaintext-boundary constant
+        # folding (plaintext boundaries only), "maj" = majority-borrow
+        # comparators (any boundaries)
+        variants = [("", False, False)] + ([("_folded", True, False)] if not enc else []) + \
+                   ([("_maj", False, True)] if name in ("cfg4", "cfg5") else [])
+        for suffix, folded, maj in variants:
             lay_full = W.PoolLayout(b)
-            units = plan(W.program_ops(b, lay_full, True, folded))["blind_rotations"]
-            run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded)
+            units = plan(W.program_ops(b, lay_full, True, folded, maj))["blind_rotations"]
+            run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj)
             run.launch()  # warm-up
             torch.cuda.synchronize()
             reps = 3 if units < 200000 else 1
@@ -373,7 +377,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
             res = run.results()
             ok = bool(res is None or np.array_equal(res, b.truth()))
             qtot = ws * Qb if scaling == "replicas" else Qb
-            out[name + ("_folded" if folded else "")] = {
+            out[name + suffix] = {
                 "queries_per_s": qtot / (ms / 1e3), "ms_per_batch": ms,
                 "queries_per_batch": qtot, "full_batch_queries": Qfull, "boxes": R, "l": l,
                 "m": m, "security_bits": sec, "encrypted_boundaries": enc,
@@ -384,7 +388,10 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                              "rank-0 combine)"}.get(name, "queries (results gathered to rank 0)"),
                 "scaling": scaling,
                 "mode": ("flagged: plaintext boundaries constant-folded (not the reference "
-                         "gate count)") if folded else "reference circuit (N(12l+2m+3) units)",
+                         "gate count)") if folded else
+                        ("flagged: majority-borrow comparators, N(4l+2m+3) units (not the "
+                         "reference gate count)") if maj else
+                        "reference circuit (N(12l+2m+3) units)",
                 "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
                                                            "(per-query cost is batch-independent "
                                                            "once the GPU is saturated)",

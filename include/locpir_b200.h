@@ -50,6 +50,8 @@ extern "C" {
 #define LOCPIR_B200_CONST 9 /* free: out = trivial sample encode_bit(in0 != 0) (gate_engine.hpp:174-179) */
 #define LOCPIR_B200_ANDNY 10 /* AND(NOT in0, in1): one bootstrap, form (-1/8, -1, +1) */
 #define LOCPIR_B200_ORNY 11  /* OR(NOT in0, in1):  one bootstrap, form (+1/8, -1, +1) */
+#define LOCPIR_B200_MAJ 12   /* MAJ(in0, in1, in2): one bootstrap of in0 + in1 + in2 (three
+                                +-1/8 never sum to 0); counted in bootstrap_units */
 
 /* Full TFHE parameter set (extends TlweParams {n, sigma}, torus.hpp:71-110). */
 typedef struct locpir_b200_params {
@@ -269,6 +271,16 @@ int locpir_b200_client_encrypt(locpir_b200_ctx* c, const uint8_t* lwe_key, uint6
  * longer applies -- hence a separate entry point).  boxes: [R][4] signed grid values
  * (x1, x2, y1, y2) of l-bit two's-complement words; results decrypt identically. */
 uint64_t locpir_b200_loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m);
+/* Flagged mode: comparators as a majority borrow chain (works with ENCRYPTED boundaries,
+ * cfg5): with the sign bits flipped, a < b = borrow out of a - b,
+ * borrow_{i+1} = MAJ(NOT a_i, b_i, borrow_i), borrow_0 = 0 -- l bootstraps per comparator
+ * instead of 3l, same depth; a region costs 4l + 2m + 3.  Same arguments as
+ * locpir_b200_loc_pir_program; decrypted results equal the reference circuit's. */
+int locpir_b200_loc_pir_maj_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                    const uint32_t* x_slots, const uint32_t* y_slots,
+                                    const uint32_t* bnd_slots, const uint32_t* svc_slots,
+                                    const uint32_t* out_slots, uint64_t scratch_first,
+                                    int xor_tree, locpir_b200_gate_op* ops, uint64_t* count);
 int locpir_b200_loc_pir_folded_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                        const uint32_t* x_slots, const uint32_t* y_slots,
                                        const int64_t* boxes, const uint32_t* svc_slots,

@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
 
 EXACT, FFT = 0, 1
 GATES = {"and": 0, "or": 1, "xor": 2, "xnor": 3, "nand": 4, "mux": 5, "not": 6, "nor": 7,
-         "andny": 10, "orny": 11}
+         "andny": 10, "orny": 11, "maj": 12}
 
 
 class GateItem(C.Structure):
@@ -302,7 +302,7 @@ class TfheKeys:
 
 
 # gate-program kinds (include/locpir_b200.h) -> oracle kinds; NOT/COPY/CONST are free
-_PROG_BOOT = {0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5, 7: 7, 10: 10, 11: 11}
+_PROG_BOOT = {0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5, 7: 7, 10: 10, 11: 11, 12: 12}
 _NOT, _COPY, _CONST = 6, 8, 9
 
 

@@ -719,6 +719,11 @@ int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
     case OR_GATE_NOR: lin2(n, 0xE0000000u, -1, a, -1, b, comb); break;
     case OR_GATE_ANDNY: lin2(n, 0xE0000000u, -1, a, 1, b, comb); break;
     case OR_GATE_ORNY: lin2(n, 0x20000000u, -1, a, 1, b, comb); break;
+    case OR_GATE_MAJ:
+        lin2(n, 0u, 1, a, 1, b, comb);
+        for (uint32_t q = 0; q <= n; q++)
+            comb[q] += c[q];
+        break;
     case OR_GATE_NOT:
         for (uint32_t q = 0; q <= n; q++)
             out[q] = 0u - a[q];

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LOCPIR_B200_LIB") or os.path.join(HERE, "liblocpir_b200.so")
 
 OK, EINVAL, ELOGIC, ECUDA, ENOMEM = 0, -1, -2, -3, -4
-AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST, ANDNY, ORNY = range(12)
+AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST, ANDNY, ORNY, MAJ = range(13)
 SLOT_NONE = 0xFFFFFFFF
 
 
@@ -72,6 +72,9 @@ SIGNATURES = [
      [_ctx, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
       C.c_uint64, C.c_int]),
     ("locpir_b200_loc_pir_program", C.c_int,
+     [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
+      C.c_uint64, C.c_int, _ops, _u64p]),
+    ("locpir_b200_loc_pir_maj_program", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
       C.c_uint64, C.c_int, _ops, _u64p]),
     ("locpir_b200_loc_pir_folded_scratch", C.c_uint64, [C.c_uint32] * 4),

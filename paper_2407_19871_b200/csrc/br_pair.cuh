@@ -64,10 +64,13 @@ __global__ void __launch_bounds__(64, 4)
     {
         const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
         const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
+        const uint32_t* a2 = it.in2 != SLOT_NONE ? pool_n + (size_t)it.in2 * dp.n_stride : nullptr;
         for (uint32_t i = t; i <= n; i += 64) {
             uint32_t v = (uint32_t)it.c0 * a0[i];
             if (a1)
                 v += (uint32_t)it.c1 * a1[i];
+            if (a2)
+                v += (uint32_t)it.c2 * a2[i];
             if (i == n)
                 v += it.off;
             S.abar[i] = (uint16_t)((v + (1u << 20)) >> 21);

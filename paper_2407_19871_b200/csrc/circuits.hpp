@@ -42,6 +42,21 @@ inline uint32_t emit_less(Emitter& e, const uint32_t* a, const uint32_t* b, uint
     return t0;
 }
 
+// Flagged comparator (majority borrow chain): with both sign bits flipped (free NOTs),
+// a < b (signed) = borrow out of a' - b'; borrow_{i+1} = MAJ(NOT a'_i, b'_i, borrow_i)
+// with borrow_0 = Enc(0) trivial.  One bootstrap per bit.  NOT a'_{l-1} = a_{l-1}.
+inline uint32_t emit_less_maj(Emitter& e, const uint32_t* a, const uint32_t* b, uint32_t l)
+{
+    uint32_t borrow = e.gate(LOCPIR_B200_CONST, 0);
+    for (uint32_t i = 0; i < l; i++) {
+        const bool sign = i + 1 == l;
+        const uint32_t na = sign ? a[i] : e.gate(LOCPIR_B200_NOT, a[i]);
+        const uint32_t bi = sign ? e.gate(LOCPIR_B200_NOT, b[i]) : b[i];
+        borrow = e.gate(LOCPIR_B200_MAJ, na, bi, borrow);
+    }
+    return borrow;
+}
+
 // hom_less_equal (circuits.hpp:212-216): NOT(b < a).
 inline uint32_t emit_less_equal(Emitter& e, const uint32_t* a, const uint32_t* b, uint32_t l)
 {
@@ -87,8 +102,14 @@ template <class SvcFn>
 inline void emit_loc_pir_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
                             uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
                             const uint32_t* bnd, SvcFn svc, const uint32_t* out,
-                            uint64_t scratch_first, int xor_tree)
+                            uint64_t scratch_first, int xor_tree, bool maj = false)
 {
+    auto lt = [&](Emitter& e, const uint32_t* a, const uint32_t* b) {
+        return maj ? emit_less_maj(e, a, b, l) : emit_less(e, a, b, l);
+    };
+    auto le = [&](Emitter& e, const uint32_t* a, const uint32_t* b) {  // NOT(b < a)
+        return e.gate(LOCPIR_B200_NOT, lt(e, b, a));
+    };
     Emitter e{&ops, scratch_first};
     std::vector<uint32_t> masked((size_t)R * m);
     for (uint32_t q = 0; q < Q; q++) {
@@ -99,10 +120,10 @@ inline void emit_loc_pir_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, u
             const uint32_t* x2 = bnd + ((size_t)r * 4 + 1) * l;
             const uint32_t* y1 = bnd + ((size_t)r * 4 + 2) * l;
             const uint32_t* y2 = bnd + ((size_t)r * 4 + 3) * l;
-            const uint32_t x_l = emit_less_equal(e, x1, x, l);
-            const uint32_t x_r = emit_less(e, x, x2, l);
-            const uint32_t y_l = emit_less_equal(e, y1, y, l);
-            const uint32_t y_r = emit_less(e, y, y2, l);
+            const uint32_t x_l = le(e, x1, x);
+            const uint32_t x_r = lt(e, x, x2);
+            const uint32_t y_l = le(e, y1, y);
+            const uint32_t y_r = lt(e, y, y2);
             const uint32_t v1 = e.gate(LOCPIR_B200_AND, x_l, x_r);
             const uint32_t v2 = e.gate(LOCPIR_B200_AND, y_l, y_r);
             const uint32_t f = e.gate(LOCPIR_B200_AND, v1, v2);
@@ -219,11 +240,11 @@ inline void emit_loc_pir_folded_fn(std::vector<locpir_b200_gate_op>& ops, uint32
 inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
                          uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
                          const uint32_t* bnd, const uint32_t* svc, const uint32_t* out,
-                         uint64_t scratch_first, int xor_tree)
+                         uint64_t scratch_first, int xor_tree, bool maj = false)
 {
     emit_loc_pir_fn(ops, Q, R, l, m, xs, ys, bnd,
                     [&](uint32_t, uint32_t r, uint32_t j) { return svc[(size_t)r * m + j]; }, out,
-                    scratch_first, xor_tree);
+                    scratch_first, xor_tree, maj);
 }
 
 inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,

@@ -811,7 +811,7 @@ int locpir_b200_debug_blind_rotate(locpir_b200_ctx* c, const uint32_t* lwe_n, ui
         pool_copy(c, 0, count, lwe_n, nullptr, cudaMemcpyHostToDevice, true);
         std::vector<BrItem> items(count);
         for (uint64_t g = 0; g < count; g++)
-            items[g] = {(uint32_t)g, SLOT_NONE, 1, 0, 0u, (uint32_t)g};
+            items[g] = {(uint32_t)g, SLOT_NONE, 1, 0, 0u, (uint32_t)g, SLOT_NONE, 0};
         if (count > c->scratch_slots) {
             c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
             c->scratch_slots = c->pool_N.n / c->dp.N_stride;
@@ -864,11 +864,11 @@ uint64_t locpir_b200_loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_
     return loc_pir_scratch(Q, R, l, m);
 }
 
-int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+static int loc_pir_program_impl(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                 const uint32_t* x_slots, const uint32_t* y_slots,
                                 const uint32_t* bnd_slots, const uint32_t* svc_slots,
                                 const uint32_t* out_slots, uint64_t scratch_first, int xor_tree,
-                                locpir_b200_gate_op* ops, uint64_t* count)
+                                locpir_b200_gate_op* ops, uint64_t* count, bool maj)
 {
     if (!count || !Q || !R || l < 2 || !m || !x_slots || !y_slots || !bnd_slots || !svc_slots ||
         !out_slots || xor_tree < 0 || xor_tree > 2)
@@ -876,7 +876,7 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
     try {
         std::vector<locpir_b200_gate_op> v;
         emit_loc_pir(v, Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
-                     scratch_first, xor_tree);
+                     scratch_first, xor_tree, maj);
         if (ops) {
             if (*count < v.size())
                 return LOCPIR_B200_EINVAL;
@@ -887,6 +887,26 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
     } catch (...) {
         return LOCPIR_B200_EINVAL;
     }
+}
+
+int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                const uint32_t* x_slots, const uint32_t* y_slots,
+                                const uint32_t* bnd_slots, const uint32_t* svc_slots,
+                                const uint32_t* out_slots, uint64_t scratch_first, int xor_tree,
+                                locpir_b200_gate_op* ops, uint64_t* count)
+{
+    return loc_pir_program_impl(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
+                                scratch_first, xor_tree, ops, count, false);
+}
+
+int locpir_b200_loc_pir_maj_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                    const uint32_t* x_slots, const uint32_t* y_slots,
+                                    const uint32_t* bnd_slots, const uint32_t* svc_slots,
+                                    const uint32_t* out_slots, uint64_t scratch_first,
+                                    int xor_tree, locpir_b200_gate_op* ops, uint64_t* count)
+{
+    return loc_pir_program_impl(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
+                                scratch_first, xor_tree, ops, count, true);
 }
 
 uint64_t locpir_b200_loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)

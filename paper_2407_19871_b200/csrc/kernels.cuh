@@ -22,12 +22,15 @@ namespace lpb {
 
 constexpr uint32_t SLOT_NONE = 0xFFFFFFFFu;
 
-// One blind rotation: combined = off + c0 * in0 + c1 * in1 (n-dim), output N-dim.
+// One blind rotation: combined = off + c0 * in0 + c1 * in1 + c2 * in2 (n-dim; in1 / in2
+// optional), output N-dim.  The third input serves the 3-input majority gate.
 struct BrItem {
     uint32_t in0, in1;
     int32_t c0, c1;
     uint32_t off;
     uint32_t out;  // N-dim scratch slot
+    uint32_t in2;
+    int32_t c2;
 };
 
 // One key switch: combined = in0 + in1 (N-dim, in1 optional) + (0, off) -> n-dim slot.
@@ -267,10 +270,13 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     {
         const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
         const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
+        const uint32_t* a2 = it.in2 != SLOT_NONE ? pool_n + (size_t)it.in2 * dp.n_stride : nullptr;
         for (uint32_t i = t; i <= n; i += 64) {
             uint32_t v = (uint32_t)it.c0 * a0[i];
             if (a1)
                 v += (uint32_t)it.c1 * a1[i];
+            if (a2)
+                v += (uint32_t)it.c2 * a2[i];
             if (i == n)
                 v += it.off;
             abar[i] = (uint16_t)((v + (1u << 20)) >> 21);  // round(v * 2N / 2^32), N = 1024
@@ -807,10 +813,13 @@ __global__ void __launch_bounds__(128 * L, 1)
     {
         const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
         const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
+        const uint32_t* a2 = it.in2 != SLOT_NONE ? pool_n + (size_t)it.in2 * dp.n_stride : nullptr;
         for (uint32_t i = threadIdx.x; i <= n; i += blockDim.x) {
             uint32_t v = (uint32_t)it.c0 * a0[i];
             if (a1)
                 v += (uint32_t)it.c1 * a1[i];
+            if (a2)
+                v += (uint32_t)it.c2 * a2[i];
             if (i == n)
                 v += it.off;
             S.abar[i] = (uint16_t)((v + (1u << 20)) >> 21);

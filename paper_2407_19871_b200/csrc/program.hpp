@@ -35,7 +35,7 @@ struct Plan {
     std::vector<std::vector<LinItem>> lin;  // per wave (run before the wave's BR)
     uint32_t scratch = 0;                   // N-dim scratch slots needed
     uint64_t n_br = 0, n_ks = 0;
-    uint64_t counts[9] = {0};               // and or xor xnor not mux nand nor units
+    uint64_t counts[10] = {0};              // and or xor xnor not mux nand nor units maj
     uint32_t waves() const { return (uint32_t)br.size(); }
 };
 
@@ -135,11 +135,11 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
         si.written = 1;
     };
     auto new_br = [&](uint32_t w, uint32_t in0, uint32_t in1, int32_t c0, int32_t c1,
-                      uint32_t off) {
+                      uint32_t off, uint32_t in2 = SLOT_NONE, int32_t c2 = 0) {
         ensure(w);
         const uint32_t id = (uint32_t)tmps.size();
         tmps.push_back({w});
-        P.br[w].push_back({in0, in1, c0, c1, off, id});
+        P.br[w].push_back({in0, in1, c0, c1, off, id, in2, c2});
         P.n_br++;
         return id;
     };
@@ -160,6 +160,20 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
             // counters: ANDNY / ORNY count as AND / OR
             static const int cidx[] = {0, 1, 2, 3, 6, -1, -1, 7, -1, -1, 0, 1};
             P.counts[cidx[op.kind]]++;
+        } else if (op.kind == LOCPIR_B200_MAJ) {
+            // 3-input majority: BS(in0 + in1 + in2) -- the sum of three +-1/8 never hits 0
+            use(op.in0);
+            use(op.in1);
+            use(op.in2);
+            def(op.out);
+            const uint32_t w =
+                std::max(std::max(ready_br(op.in0), ready_br(op.in1)), ready_br(op.in2));
+            const uint32_t id = new_br(w, op.in0, op.in1, 1, 1, 0u, op.in2, 1);
+            P.ks[w].push_back({id, SLOT_NONE, 0u, op.out});
+            tmps[id].wave_ks = w;
+            P.n_ks++;
+            st[op.out].rbr = st[op.out].rlin = w + 1;
+            P.counts[9]++;
         } else if (op.kind == LOCPIR_B200_MUX) {
             use(op.in0);
             use(op.in1);
@@ -197,7 +211,7 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
         }
     }
     P.counts[8] = P.counts[0] + P.counts[1] + P.counts[2] + P.counts[3] + P.counts[6] +
-                  P.counts[7] + 2 * P.counts[5];
+                  P.counts[7] + 2 * P.counts[5] + P.counts[9];
 
     // assign N-dim scratch slots: a value lives from its BR wave to its KS wave
     std::vector<uint32_t> phys(tmps.size(), SLOT_NONE), freelist;

@@ -145,7 +145,7 @@ class ShardedLocPir:
     evaluates its query shard against all boxes; outputs are gathered to rank 0.
     Every rank holds the same seeded batch `b` (inputs are encrypted deterministically)."""
 
-    def __init__(self, backend, b, rank, world, mode, seed, folded=False):
+    def __init__(self, backend, b, rank, world, mode, seed, folded=False, maj=False):
         from . import workloads as W
         self.be, self.b, self.rank, self.world, self.mode = backend, b, rank, world, mode
         Q, R, m = b.Q, b.R, b.m
@@ -176,7 +176,7 @@ class ShardedLocPir:
         backend.reserve(total)
         if self.sub is not None:
             backend.load(self.sub, self.lay, seed)
-            self.prog = backend.program(W.program_ops(self.sub, self.lay, tree, folded))
+            self.prog = backend.program(W.program_ops(self.sub, self.lay, tree, folded, maj))
         if rank == 0 and mode == "boxes" and world > 1:
             self.combine = backend.program(W.combine_ops(self.G, Q, m, self.part_first,
                                                          self.out_first, self.comb_first))

@@ -394,16 +394,18 @@ def _tree_mode(xor_tree) -> int:
 
 
 def loc_pir_program(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
-                    scratch_first, xor_tree=True):
-    """Host-only emission of the loc_pir gate program."""
+                    scratch_first, xor_tree=True, maj=False):
+    """Host-only emission of the loc_pir gate program (maj=True: flagged majority-borrow
+    comparators, locpir_b200_loc_pir_maj_program)."""
     arrs = [np.ascontiguousarray(v, np.uint32).reshape(-1)
             for v in (x_slots, y_slots, bnd_slots, svc_slots, out_slots)]
     cnt = C.c_uint64(0)
-    _check(lib().locpir_b200_loc_pir_program(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first,
-                                             _tree_mode(xor_tree), None, C.byref(cnt)))
+    fn = lib().locpir_b200_loc_pir_maj_program if maj else lib().locpir_b200_loc_pir_program
+    _check(fn(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first, _tree_mode(xor_tree), None,
+              C.byref(cnt)))
     ops = (GateOp * cnt.value)()
-    _check(lib().locpir_b200_loc_pir_program(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first,
-                                             _tree_mode(xor_tree), ops, C.byref(cnt)))
+    _check(fn(Q, R, l, m, *[_u32(v) for v in arrs], scratch_first, _tree_mode(xor_tree), ops,
+              C.byref(cnt)))
     return ops
 
 

@@ -114,9 +114,10 @@ def signed_boxes(b: LocPirBatch) -> np.ndarray:
     return b.boxes.astype(np.int64) - (1 << (b.l - 1))
 
 
-def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False):
+def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False):
     """folded=True: flagged plaintext-boundary mode; not for cfg5,
-    whose boundaries are encrypted."""
+    whose boundaries are encrypted.  maj=True: flagged majority-borrow comparators (any
+    boundaries)."""
     from .engine import loc_pir_folded_program, loc_pir_program
     if folded:
         if b.encrypted_bounds:
@@ -124,11 +125,11 @@ def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False):
         return loc_pir_folded_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, signed_boxes(b),
                                       lay.svc, lay.out, lay.scratch, xor_tree)
     return loc_pir_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.bnd, lay.svc, lay.out,
-                           lay.scratch, xor_tree)
+                           lay.scratch, xor_tree, maj)
 
 
-def program(ctx, b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False):
-    return ctx.program(program_ops(b, lay, xor_tree, folded))
+def program(ctx, b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False):
+    return ctx.program(program_ops(b, lay, xor_tree, folded, maj))
 
 
 def read_results(ctx, keys, b: LocPirBatch, lay: PoolLayout) -> np.ndarray:

@@ -14,6 +14,7 @@ _F = {
     _abi.MUX: lambda a, b, c: b if a else c, _abi.NOT: lambda a, b, c: 1 - a,
     _abi.COPY: lambda a, b, c: a, _abi.ANDNY: lambda a, b, c: (1 - a) & b,
     _abi.ORNY: lambda a, b, c: (1 - a) | b,
+    _abi.MAJ: lambda a, b, c: 1 if a + b + c >= 2 else 0,
 }
 
 

@@ -19,6 +19,7 @@ def interpret(ops, pool):
         _abi.MUX: lambda a, b, c: b if a else c, _abi.NOT: lambda a, b, c: 1 - a,
         _abi.COPY: lambda a, b, c: a, _abi.ANDNY: lambda a, b, c: (1 - a) & b,
         _abi.ORNY: lambda a, b, c: (1 - a) | b,
+        _abi.MAJ: lambda a, b, c: 1 if a + b + c >= 2 else 0,
     }
     for op in ops:
         if op.kind == _abi.CONST:
@@ -29,7 +30,7 @@ def interpret(ops, pool):
     return pool
 
 
-def run_plain(b, folded, xor_tree=True):
+def run_plain(b, folded, xor_tree=True, maj=False):
     lay = W.PoolLayout(b)
     pool = {}
     l, m = b.l, b.m
@@ -45,7 +46,7 @@ def run_plain(b, folded, xor_tree=True):
                 pool[int(lay.bnd[r, k, i])] = int(bb[r, k, i])
         for j in range(m):
             pool[int(lay.svc[r, j])] = int((int(b.payload[r]) >> j) & 1)
-    ops = W.program_ops(b, lay, xor_tree, folded)
+    ops = W.program_ops(b, lay, xor_tree, folded, maj)
     interpret(ops, pool)
     out = np.zeros(b.Q, np.uint64)
     for q in range(b.Q):
