@@ -432,6 +432,10 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 // warp (all lanes work on the same ciphertext), so the row choice is a
 // warp-uniform branch and each selected row costs one add per column.
 // ---------------------------------------------------------------------------
+#ifndef KS_JUNROLL
+#define KS_JUNROLL 1
+#endif
+constexpr int kKsJUnroll = KS_JUNROLL;  // digit-position loop unrolling (icache vs ILP)
 #ifndef KS_PREFETCH
 #define KS_PREFETCH 1
 #endif
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
 #pragma unroll
         for (int c = 0; c < KS_CT / 2; c++)
             dw[c] = dp32[c];  // broadcast: two ciphertexts' digit words
-#pragma unroll
+#pragma unroll kKsJUnroll
         for (int j = 0; j < 8; j++) {
 #if KS_PREFETCH
             // rows of step (i, j) were loaded one step ahead; issue step (i, j+1) now
