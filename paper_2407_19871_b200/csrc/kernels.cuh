@@ -873,7 +873,11 @@ __global__ void __launch_bounds__(128 * L, 1)
                 for (int k = 0; k < P; k++) {
                     const int q = msub + L * k;
                     if (q < 8)
+#if LAT_SKIP_BK
+                        bkv[r][k] = make_double2(1.0 + r, 0.5 * k);
+#else
                         bkv[r][k] = ld_stream(bki + (size_t)r * 2 * FFT_M + q * 64 + t);
+#endif
                 }
         }
         // every group: digit (c, p) of (X^a - 1) ACC_c -> forward transform -> F[g]
