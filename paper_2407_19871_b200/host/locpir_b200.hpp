@@ -116,10 +116,11 @@ private:
 struct GateCounterSnapshot {
     uint64_t and_gates = 0, or_gates = 0, xor_gates = 0, xnor_gates = 0, not_gates = 0,
              mux_gates = 0, nand_gates = 0, nor_gates = 0;
+    uint64_t other_units = 0;  // flagged single-bootstrap gates outside the reference set (MAJ)
     uint64_t bootstrap_units() const  // gate_engine.hpp:44-48 (+ NAND/NOR)
     {
         return and_gates + or_gates + xor_gates + xnor_gates + nand_gates + nor_gates +
-               2 * mux_gates;
+               2 * mux_gates + other_units;
     }
     std::map<std::string, uint64_t> as_map() const
     {
@@ -149,7 +150,9 @@ public:
         const_cast<GateEngine*>(this)->flush();
         uint64_t c[9];
         check(locpir_b200_counters(st_->ctx, c), st_->ctx);
-        return {c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]};
+        GateCounterSnapshot snap{c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7]};
+        snap.other_units = c[8] - snap.bootstrap_units();  // the library's unit total
+        return snap;
     }
     void reset_counters() { check(locpir_b200_counters_reset(st_->ctx), st_->ctx); }
 
@@ -187,6 +190,18 @@ public:
     CipherBit hom_mux(const CipherBit& s, const CipherBit& a, const CipherBit& b)
     {
         return emit(LOCPIR_B200_MUX, slot(s), slot(a), slot(b));
+    }
+    // 3-input majority in ONE bootstrap (flagged comparator mode; not in the reference)
+    CipherBit hom_maj(const CipherBit& a, const CipherBit& b, const CipherBit& c)
+    {
+        return emit(LOCPIR_B200_MAJ, slot(a), slot(b), slot(c));
+    }
+
+    // the context behind this engine (for BatchingServer and other C-ABI users)
+    locpir_b200_ctx* native()
+    {
+        flush();
+        return st_->ctx;
     }
 
     // -- level batching ---------------------------------------------------------
@@ -365,19 +380,42 @@ inline ServiceCiphertext xor_sum_services(const std::vector<ServiceCiphertext>& 
     return out;
 }
 
+// Flagged comparator: a < b = borrow out of a' - b' with both sign bits flipped,
+// borrow_{i+1} = MAJ(NOT a'_i, b'_i, borrow_i): l bootstraps instead of 3l.
+inline CipherBit hom_less_maj(const CipherWord& a, const CipherWord& b, GateEngine& e)
+{
+    if (a.bits.size() != b.bits.size() || a.bits.empty())
+        throw std::invalid_argument("comparator operands must share length and format");
+    BatchScope scope(e);
+    const size_t l = a.bits.size();
+    CipherBit borrow = e.constant(false);
+    for (size_t i = 0; i < l; i++) {
+        const bool sign = i + 1 == l;
+        const CipherBit na = sign ? a.bits[i] : e.hom_not(a.bits[i]);
+        const CipherBit bi = sign ? e.hom_not(b.bits[i]) : b.bits[i];
+        borrow = e.hom_maj(na, bi, borrow);
+    }
+    return borrow;
+}
+
+enum class Comparator { Reference, Majority };
+
 inline ServiceCiphertext loc_pir(const CipherWord& x, const CipherWord& y,
                                  const std::vector<EncodedRegion>& regions, GateEngine& e,
-                                 bool tree = true)
+                                 bool tree = true, Comparator cmp = Comparator::Reference)
 {
     if (regions.empty())
         return {};
     BatchScope scope(e);
+    auto lt = [&](const CipherWord& a, const CipherWord& b) {
+        return cmp == Comparator::Majority ? hom_less_maj(a, b, e) : hom_less(a, b, e);
+    };
     std::vector<ServiceCiphertext> masked;
     for (const EncodedRegion& r : regions) {
-        const CipherBit x_l = hom_less_equal(r.x1, x, e);
-        const CipherBit x_r = hom_less(x, r.x2, e);
-        const CipherBit y_l = hom_less_equal(r.y1, y, e);
-        const CipherBit y_r = hom_less(y, r.y2, e);
+        const CipherBit x_l = e.hom_not(lt(x, r.x1));
+        const CipherBit x_r = lt(x, r.x2);
+        const CipherBit y_l = e.hom_not(lt(y, r.y1));
+        const CipherBit y_r = lt(y, r.y2);
         const CipherBit v1 = e.hom_and(x_l, x_r);
         const CipherBit v2 = e.hom_and(y_l, y_r);
         const CipherBit f = e.hom_and(v1, v2);
@@ -385,5 +423,69 @@ inline ServiceCiphertext loc_pir(const CipherWord& x, const CipherWord& y,
     }
     return xor_sum_services(masked, e, tree);
 }
+
+// ---- cross-session query batcher (csrc/server.hpp) ---------------------
+// Server::handle_zerosheet / handle_query (protocol.hpp:373-424) without the transport:
+// wire payloads in, RESPONSE payloads out, one batched program per flush().
+class BatchingServer {
+public:
+    BatchingServer(GateEngine& eng, const std::vector<int64_t>& boxes /* [R][4] grid */,
+                   const std::vector<uint64_t>& services, uint32_t l, uint32_t m,
+                   uint32_t max_sessions = 64, bool folded = false)
+        : m_(m), n_(eng.params().n())
+    {
+        if (boxes.size() != services.size() * 4)
+            throw std::invalid_argument("one service value per box");
+        locpir_b200_ctx* c = eng.native();
+        check(locpir_b200_server_create(c, boxes.data(), services.data(), (uint32_t)services.size(),
+                                        l, m, max_sessions, folded ? 1 : 0, &s_),
+              c);
+    }
+    ~BatchingServer() { locpir_b200_server_destroy(s_); }
+    BatchingServer(const BatchingServer&) = delete;
+    BatchingServer& operator=(const BatchingServer&) = delete;
+
+    uint32_t open_session(const std::vector<uint8_t>& zero_sheet)
+    {
+        uint32_t id = 0;
+        ck(locpir_b200_server_open_session(s_, zero_sheet.data(), zero_sheet.size(), &id));
+        return id;
+    }
+    void close_session(uint32_t id) { ck(locpir_b200_server_close_session(s_, id)); }
+    uint64_t submit(uint32_t session, const std::vector<uint8_t>& query)
+    {
+        uint64_t t = 0;
+        ck(locpir_b200_server_submit(s_, session, query.data(), query.size(), &t));
+        return t;
+    }
+    uint64_t pending() const { return locpir_b200_server_pending(s_); }
+    uint64_t flush()
+    {
+        uint64_t n = 0;
+        ck(locpir_b200_server_flush(s_, &n));
+        return n;
+    }
+    std::vector<uint8_t> take_response(uint64_t ticket)
+    {
+        std::vector<uint8_t> out((size_t)m_ * 4 * (n_ + 1));
+        ck(locpir_b200_server_take_response(s_, ticket, out.data(), out.size()));
+        return out;
+    }
+
+private:
+    void ck(int rc)
+    {
+        if (rc == LOCPIR_B200_OK)
+            return;
+        const std::string msg = locpir_b200_server_last_error(s_);
+        if (rc == LOCPIR_B200_EINVAL)
+            throw std::invalid_argument(msg);
+        if (rc == LOCPIR_B200_ELOGIC)
+            throw std::logic_error(msg);
+        throw std::runtime_error(msg);
+    }
+    locpir_b200_server* s_ = nullptr;
+    uint32_t m_, n_;
+};
 
 }  // namespace locpir_b200

@@ -3,6 +3,7 @@
 // Mirrors test_gate_engine.cpp:17-97 and test_circuits.cpp:26-213 (Catch2 is not in
 // this image; a tiny CHECK macro stands in).  Driven by tests/test_cpp_mirror.py.
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <functional>
 #include <stdexcept>
@@ -113,6 +114,7 @@ int main()
         const int l = 6;
         const int64_t vals[] = {-32, -17, -1, 0, 1, 17, 31};
         std::vector<std::tuple<int64_t, int64_t, CipherBit, CipherBit>> res;
+        std::vector<std::tuple<int64_t, int64_t, CipherBit>> majres;
         {
             std::vector<std::pair<CipherWord, CipherWord>> words;
             for (int64_t a : vals)
@@ -125,12 +127,15 @@ int main()
                     const auto& w = words[k++];
                     res.emplace_back(a, b, hom_less(w.first, w.second, eng),
                                      hom_less_equal(w.first, w.second, eng));
+                    majres.emplace_back(a, b, hom_less_maj(w.first, w.second, eng));
                 }
         }
         for (auto& [a, b, lt, le] : res) {
             CHECK(eng.decrypt(lt) == (a < b));
             CHECK(eng.decrypt(le) == (a <= b));
         }
+        for (auto& [a, b, lt] : majres)  // flagged majority-borrow comparator
+            CHECK(eng.decrypt(lt) == (a < b));
     }
 
     // test_circuits.cpp:150-213 loc_pir retrieval, half-open edges, counts
@@ -167,6 +172,69 @@ int main()
         CHECK(s.xnor_gates == q * N * 4 * l && s.mux_gates == q * N * 4 * l);
         CHECK(s.and_gates == q * N * (3 + m) && s.xor_gates == q * N * m);
         CHECK(s.bootstrap_units() == q * N * (12 * l + 2 * m + 3));
+        eng.reset_counters();
+        for (const auto& [pt, want] : cases) {  // flagged majority comparators: same answers
+            const CipherWord x = enc_int(pt.first, l, eng), y = enc_int(pt.second, l, eng);
+            CHECK(dec_service(loc_pir(x, y, regions, eng, true, Comparator::Majority), eng) == want);
+        }
+        CHECK(eng.counters().bootstrap_units() == 8 * N * (4 * l + 2 * m + 3));
+    }
+
+    // majority gate truth table (one bootstrap of a + b + c)
+    for (int a = 0; a <= 1; a++)
+        for (int b = 0; b <= 1; b++)
+            for (int c = 0; c <= 1; c++) {
+                const CipherBit ca = eng.encrypt(a), cb = eng.encrypt(b), cc = eng.encrypt(c);
+                CHECK(eng.decrypt(eng.hom_maj(ca, cb, cc)) == (a + b + c >= 2));
+            }
+
+    // cross-session batcher through wire payloads (protocol.hpp:185-227)
+    {
+        const uint32_t l = 16, m = 4;
+        const std::vector<int64_t> boxes = {0, 100, 0, 100, -50, 20, -30, 10, 200, 300, -5, 5};
+        const std::vector<uint64_t> services = {9, 6, 13};
+        BatchingServer srv(eng, boxes, services, l, m, 2);
+        const size_t S = keys.params.sample_words();
+        auto sheet = [&](uint64_t seed) {  // Enc(-1/8) + 1/8 = Enc(0) per sample
+            auto cts = keys.encrypt(std::vector<uint8_t>(services.size() * m, 0), seed);
+            for (size_t i = 0; i < services.size() * m; i++)
+                cts[i * S + S - 1] += 0x20000000u;
+            std::vector<uint8_t> b(cts.size() * 4);
+            std::memcpy(b.data(), cts.data(), b.size());
+            return b;
+        };
+        const uint32_t s0 = srv.open_session(sheet(501)), s1 = srv.open_session(sheet(502));
+        auto query = [&](int64_t gx, int64_t gy, uint64_t seed) {
+            std::vector<uint8_t> out;
+            for (int64_t g : {gx, gy}) {
+                std::vector<uint8_t> bits(l);
+                for (uint32_t i = 0; i < l; i++)
+                    bits[i] = ((uint64_t)g >> i) & 1;
+                const auto cts = keys.encrypt(bits, seed++);
+                out.push_back((uint8_t)l);
+                const uint8_t* p = reinterpret_cast<const uint8_t*>(cts.data());
+                out.insert(out.end(), p, p + cts.size() * 4);
+            }
+            return out;
+        };
+        const std::pair<std::pair<int64_t, int64_t>, uint64_t> qs[] = {
+            {{50, 50}, 9}, {{0, -30}, 6}, {{250, 0}, 13}, {{-60, 0}, 0}, {{19, 9}, 6 ^ 9}};
+        std::vector<uint64_t> tickets;
+        uint64_t seed = 600;
+        for (size_t i = 0; i < 5; i++, seed += 2)
+            tickets.push_back(srv.submit(i % 2 ? s1 : s0, query(qs[i].first.first, qs[i].first.second, seed)));
+        CHECK(srv.pending() == 5 && srv.flush() == 5);
+        for (size_t i = 0; i < 5; i++) {
+            const auto resp = srv.take_response(tickets[i]);
+            std::vector<uint32_t> w(resp.size() / 4);
+            std::memcpy(w.data(), resp.data(), resp.size());
+            const auto bits = keys.decrypt(w);
+            uint64_t v = 0;
+            for (uint32_t j = 0; j < m; j++)
+                v |= (uint64_t)bits[j] << j;
+            CHECK(v == qs[i].second);
+        }
+        CHECK_THROWS_AS(srv.submit(7, query(1, 1, 9)), std::logic_error);
     }
 
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
