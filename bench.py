@@ -385,12 +385,18 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
         # flagged modes (not the reference count): "folded" = plaintext-boundary constant
         # folding (plaintext boundaries only), "maj" = majority-borrow
         # comparators (any boundaries)
-        variants = [("", False, False)] + ([("_folded", True, False)] if not enc else []) + \
-                   ([("_maj", False, True)] if name in ("cfg4", "cfg5") else [])
-        for suffix, folded, maj in variants:
+        # "tree" = log-depth comparators (latency mode, for the single-query cfg1)
+        variants = [("", False, False, False)] + \
+                   ([("_folded", True, False, False)] if not enc else []) + \
+                   ([("_maj", False, True, False)] if name in ("cfg4", "cfg5") else []) + \
+                   ([("_tree", True, False, True)] if name == "cfg1" else [])
+        for suffix, folded, maj, tree in variants:
             lay_full = W.PoolLayout(b)
-            units = plan(W.program_ops(b, lay_full, True, folded, maj))["blind_rotations"]
-            run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj)
+            ops_full = W.program_ops(b, lay_full, True, folded, maj, tree)
+            pl = plan(ops_full)
+            units = pl["blind_rotations"]
+            run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj,
+                                tree=tree)
             run.launch()  # warm-up
             torch.cuda.synchronize()
             reps = 3 if units < 200000 else 1
@@ -415,7 +421,10 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                 "sharding": {"cfg1": "replicas", "cfg3": "boxes (partial roots all-gathered, "
                              "rank-0 combine)"}.get(name, "queries (results gathered to rank 0)"),
                 "scaling": scaling,
-                "mode": ("flagged: plaintext boundaries constant-folded (not the reference "
+                "levels": pl["levels"],
+                "mode": ("flagged: folded log-depth tree comparators, latency mode (not the "
+                         "reference gate count)") if tree else
+                        ("flagged: plaintext boundaries constant-folded (not the reference "
                          "gate count)") if folded else
                         ("flagged: majority-borrow comparators, N(4l+2m+3) units (not the "
                          "reference gate count)") if maj else

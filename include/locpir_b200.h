@@ -281,6 +281,19 @@ int locpir_b200_loc_pir_maj_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t
                                     const uint32_t* bnd_slots, const uint32_t* svc_slots,
                                     const uint32_t* out_slots, uint64_t scratch_first,
                                     int xor_tree, locpir_b200_gate_op* ops, uint64_t* count);
+/* General emitter.  Exactly one of bnd_slots ([R][4][l] pool slots, as
+ * locpir_b200_loc_pir_program) or boxes ([R][4] plaintext signed grid values, folded as
+ * locpir_b200_loc_pir_folded_program) is non-NULL.  comparator: 0 = reference XNOR/MUX
+ * chain (folded chain for plaintext boxes), 1 = majority borrow chain (slots only),
+ * 2 = log-depth tree (flagged latency mode: depth log2 l, +1 with encrypted boundaries,
+ * more gates; for latency-bound batches such as cfg1).  Scratch: locpir_b200_loc_pir_scratch
+ * bounds every mode. */
+int locpir_b200_loc_pir_program_ex(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                   const uint32_t* x_slots, const uint32_t* y_slots,
+                                   const uint32_t* bnd_slots, const int64_t* boxes,
+                                   const uint32_t* svc_slots, const uint32_t* out_slots,
+                                   uint64_t scratch_first, int xor_tree, int comparator,
+                                   locpir_b200_gate_op* ops, uint64_t* count);
 int locpir_b200_loc_pir_folded_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                        const uint32_t* x_slots, const uint32_t* y_slots,
                                        const int64_t* boxes, const uint32_t* svc_slots,

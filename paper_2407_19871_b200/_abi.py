@@ -77,6 +77,9 @@ SIGNATURES = [
     ("locpir_b200_loc_pir_maj_program", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, _u32p, _u32p,
       C.c_uint64, C.c_int, _ops, _u64p]),
+    ("locpir_b200_loc_pir_program_ex", C.c_int,
+     [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, _u32p, C.POINTER(C.c_int64),
+      _u32p, _u32p, C.c_uint64, C.c_int, C.c_int, _ops, _u64p]),
     ("locpir_b200_loc_pir_folded_scratch", C.c_uint64, [C.c_uint32] * 4),
     ("locpir_b200_loc_pir_folded_program", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.POINTER(C.c_int64), _u32p,

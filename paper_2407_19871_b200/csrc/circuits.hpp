@@ -57,6 +57,89 @@ inline uint32_t emit_less_maj(Emitter& e, const uint32_t* a, const uint32_t* b, 
     return borrow;
 }
 
+// ---- flagged latency mode: log-depth (tree) comparator ------------------------------
+// Same function as hom_less.  With both sign bits flipped, per bit
+//   lt_i = NOT a'_i AND b'_i,  eq_i = (a'_i == b'_i)
+// and pairs merge up a balanced tree (hi = the more significant half):
+//   lt = eq_hi ? lt_lo : lt_hi   (MUX; lt_hi and eq_hi are exclusive)
+//   eq = eq_hi AND eq_lo
+// Depth log2(l) (+1 with an encrypted b) instead of l, for latency-bound batches (cfg1).
+// b bits may be plaintext constants (folded) or pool slots; constants propagate for free.
+struct TBit {
+    bool is_const;
+    int v;
+    uint32_t slot;
+    static TBit c(int x) { return {true, x ? 1 : 0, 0}; }
+    static TBit s(uint32_t x) { return {false, 0, x}; }
+};
+
+struct TreeOps {
+    Emitter& e;
+    uint32_t mat(TBit x) { return x.is_const ? e.gate(LOCPIR_B200_CONST, (uint32_t)x.v) : x.slot; }
+    TBit not_(TBit x) { return x.is_const ? TBit::c(!x.v) : TBit::s(e.gate(LOCPIR_B200_NOT, x.slot)); }
+    TBit and_(TBit x, TBit y)
+    {
+        if ((x.is_const && !x.v) || (y.is_const && !y.v))
+            return TBit::c(0);
+        if (x.is_const)
+            return y;
+        if (y.is_const)
+            return x;
+        return TBit::s(e.gate(LOCPIR_B200_AND, x.slot, y.slot));
+    }
+    TBit mux(TBit s_, TBit a, TBit b)  // s ? a : b
+    {
+        if (s_.is_const)
+            return s_.v ? a : b;
+        if (a.is_const && b.is_const)
+            return a.v == b.v ? a : (a.v ? s_ : not_(s_));
+        if (a.is_const)  // s ? 1 : b = s OR b ; s ? 0 : b = NOT s AND b
+            return TBit::s(e.gate(a.v ? LOCPIR_B200_OR : LOCPIR_B200_ANDNY, s_.slot, b.slot));
+        if (b.is_const)  // s ? a : 1 = NOT s OR a ; s ? a : 0 = s AND a
+            return TBit::s(e.gate(b.v ? LOCPIR_B200_ORNY : LOCPIR_B200_AND, s_.slot, a.slot));
+        return TBit::s(e.gate(LOCPIR_B200_MUX, s_.slot, a.slot, b.slot));
+    }
+};
+
+// a: l slots; b: l TBits (constants or slots).  Returns the slot of a < b (signed).
+inline uint32_t emit_less_tree(Emitter& e, const uint32_t* a, const TBit* b, uint32_t l)
+{
+    TreeOps t{e};
+    std::vector<TBit> lt(l), eq(l);
+    for (uint32_t i = 0; i < l; i++) {
+        const bool sign = i + 1 == l;
+        TBit ai = TBit::s(a[i]);
+        TBit bi = b[i];
+        // a'_i = NOT a_{l-1} at the sign position (free); NOT a'_i is then a_{l-1}
+        const TBit na = sign ? ai : t.not_(ai);
+        const TBit ap = sign ? t.not_(ai) : ai;
+        if (sign)
+            bi = t.not_(bi);
+        if (bi.is_const) {
+            lt[i] = bi.v ? na : TBit::c(0);
+            eq[i] = bi.v ? ap : na;
+        } else {
+            lt[i] = TBit::s(e.gate(LOCPIR_B200_ANDNY, t.mat(ap), bi.slot));
+            eq[i] = TBit::s(e.gate(LOCPIR_B200_XNOR, t.mat(ap), bi.slot));
+        }
+    }
+    // merge [lo, hi) ranges bottom-up; level vectors hold (lt, eq) of consecutive groups
+    while (lt.size() > 1) {
+        std::vector<TBit> nlt, neq;
+        for (size_t i = 0; i + 1 < lt.size(); i += 2) {
+            nlt.push_back(t.mux(eq[i + 1], lt[i], lt[i + 1]));
+            neq.push_back(lt.size() == 2 ? TBit::c(0) : t.and_(eq[i + 1], eq[i]));
+        }
+        if (lt.size() & 1) {
+            nlt.push_back(lt.back());
+            neq.push_back(eq.back());
+        }
+        lt.swap(nlt);
+        eq.swap(neq);
+    }
+    return t.mat(lt[0]);
+}
+
 // hom_less_equal (circuits.hpp:212-216): NOT(b < a).
 inline uint32_t emit_less_equal(Emitter& e, const uint32_t* a, const uint32_t* b, uint32_t l)
 {
@@ -65,9 +148,10 @@ inline uint32_t emit_less_equal(Emitter& e, const uint32_t* a, const uint32_t* b
 
 inline uint64_t loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
 {
-    // per region: 4 comparators x (2 NOT + 1 CONST + 2l) + 2 NOT + 3 AND + m AND;
-    // per query and bit column: 1 CONST + (R - 1) XOR
-    const uint64_t per_region = 4ull * (3 + 2ull * l) + 2 + 3 + m;
+    // per region: 4 comparators x (at most 7l + 4 slots: the reference chain needs
+    // 2 NOT + 1 CONST + 2l, the majority chain 2l + 1, the tree 5l) + 2 NOT + 3 AND +
+    // m AND; per query and bit column: 1 CONST + (R - 1) XOR
+    const uint64_t per_region = 4ull * (4 + 7ull * l) + 2 + 3 + m;
     const uint64_t per_query = (uint64_t)R * per_region + (uint64_t)m * (1 + R);
     return (uint64_t)Q * per_query;
 }
@@ -102,10 +186,19 @@ template <class SvcFn>
 inline void emit_loc_pir_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
                             uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
                             const uint32_t* bnd, SvcFn svc, const uint32_t* out,
-                            uint64_t scratch_first, int xor_tree, bool maj = false)
+                            uint64_t scratch_first, int xor_tree, int cmp = 0)
 {
+    // cmp: 0 = reference XNOR/MUX chain, 1 = majority borrow chain, 2 = log-depth tree
+    std::vector<TBit> tb(l);
     auto lt = [&](Emitter& e, const uint32_t* a, const uint32_t* b) {
-        return maj ? emit_less_maj(e, a, b, l) : emit_less(e, a, b, l);
+        if (cmp == 1)
+            return emit_less_maj(e, a, b, l);
+        if (cmp == 2) {
+            for (uint32_t i = 0; i < l; i++)
+                tb[i] = TBit::s(b[i]);
+            return emit_less_tree(e, a, tb.data(), l);
+        }
+        return emit_less(e, a, b, l);
     };
     auto le = [&](Emitter& e, const uint32_t* a, const uint32_t* b) {  // NOT(b < a)
         return e.gate(LOCPIR_B200_NOT, lt(e, b, a));
@@ -191,7 +284,8 @@ inline uint32_t emit_less_plain(Emitter& e, const uint32_t* a, int64_t B, uint32
 
 inline uint64_t loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
 {
-    const uint64_t per_region = 4ull * (l + 2) + 2 + 3 + m;
+    // per comparator: the folded chain needs l + 2 slots, the folded tree at most 4l + 1
+    const uint64_t per_region = 4ull * (4ull * l + 2) + 2 + 3 + m;
     return (uint64_t)Q * ((uint64_t)R * per_region + (uint64_t)m * (1 + R));
 }
 
@@ -200,8 +294,16 @@ template <class SvcFn>
 inline void emit_loc_pir_folded_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
                                    uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
                                    const int64_t* boxes, SvcFn svc, const uint32_t* out,
-                                   uint64_t scratch_first, int xor_tree)
+                                   uint64_t scratch_first, int xor_tree, bool tree = false)
 {
+    std::vector<TBit> tb(l);
+    auto lt_plain = [&](Emitter& e, const uint32_t* a, int64_t B) {
+        if (!tree)
+            return emit_less_plain(e, a, B, l);
+        for (uint32_t i = 0; i < l; i++)
+            tb[i] = TBit::c((int)(((uint64_t)B >> i) & 1));
+        return emit_less_tree(e, a, tb.data(), l);
+    };
     Emitter e{&ops, scratch_first};
     std::vector<uint32_t> masked((size_t)R * m);
     for (uint32_t q = 0; q < Q; q++) {
@@ -209,10 +311,10 @@ inline void emit_loc_pir_folded_fn(std::vector<locpir_b200_gate_op>& ops, uint32
         const uint32_t* y = ys + (size_t)q * l;
         for (uint32_t r = 0; r < R; r++) {
             const int64_t* bx = boxes + (size_t)r * 4;
-            const uint32_t x_l = e.gate(LOCPIR_B200_NOT, emit_less_plain(e, x, bx[0], l));
-            const uint32_t x_r = emit_less_plain(e, x, bx[1], l);
-            const uint32_t y_l = e.gate(LOCPIR_B200_NOT, emit_less_plain(e, y, bx[2], l));
-            const uint32_t y_r = emit_less_plain(e, y, bx[3], l);
+            const uint32_t x_l = e.gate(LOCPIR_B200_NOT, lt_plain(e, x, bx[0]));
+            const uint32_t x_r = lt_plain(e, x, bx[1]);
+            const uint32_t y_l = e.gate(LOCPIR_B200_NOT, lt_plain(e, y, bx[2]));
+            const uint32_t y_r = lt_plain(e, y, bx[3]);
             const uint32_t v1 = e.gate(LOCPIR_B200_AND, x_l, x_r);
             const uint32_t v2 = e.gate(LOCPIR_B200_AND, y_l, y_r);
             const uint32_t f = e.gate(LOCPIR_B200_AND, v1, v2);
@@ -240,21 +342,21 @@ inline void emit_loc_pir_folded_fn(std::vector<locpir_b200_gate_op>& ops, uint32
 inline void emit_loc_pir(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
                          uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
                          const uint32_t* bnd, const uint32_t* svc, const uint32_t* out,
-                         uint64_t scratch_first, int xor_tree, bool maj = false)
+                         uint64_t scratch_first, int xor_tree, int cmp = 0)
 {
     emit_loc_pir_fn(ops, Q, R, l, m, xs, ys, bnd,
                     [&](uint32_t, uint32_t r, uint32_t j) { return svc[(size_t)r * m + j]; }, out,
-                    scratch_first, xor_tree, maj);
+                    scratch_first, xor_tree, cmp);
 }
 
 inline void emit_loc_pir_folded(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, uint32_t R,
                                 uint32_t l, uint32_t m, const uint32_t* xs, const uint32_t* ys,
                                 const int64_t* boxes, const uint32_t* svc, const uint32_t* out,
-                                uint64_t scratch_first, int xor_tree)
+                                uint64_t scratch_first, int xor_tree, bool tree = false)
 {
     emit_loc_pir_folded_fn(ops, Q, R, l, m, xs, ys, boxes,
                            [&](uint32_t, uint32_t r, uint32_t j) { return svc[(size_t)r * m + j]; },
-                           out, scratch_first, xor_tree);
+                           out, scratch_first, xor_tree, tree);
 }
 
 }  // namespace lpb

@@ -868,7 +868,7 @@ static int loc_pir_program_impl(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                 const uint32_t* x_slots, const uint32_t* y_slots,
                                 const uint32_t* bnd_slots, const uint32_t* svc_slots,
                                 const uint32_t* out_slots, uint64_t scratch_first, int xor_tree,
-                                locpir_b200_gate_op* ops, uint64_t* count, bool maj)
+                                locpir_b200_gate_op* ops, uint64_t* count, int cmp)
 {
     if (!count || !Q || !R || l < 2 || !m || !x_slots || !y_slots || !bnd_slots || !svc_slots ||
         !out_slots || xor_tree < 0 || xor_tree > 2)
@@ -876,7 +876,7 @@ static int loc_pir_program_impl(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
     try {
         std::vector<locpir_b200_gate_op> v;
         emit_loc_pir(v, Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
-                     scratch_first, xor_tree, maj);
+                     scratch_first, xor_tree, cmp);
         if (ops) {
             if (*count < v.size())
                 return LOCPIR_B200_EINVAL;
@@ -896,7 +896,7 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                 locpir_b200_gate_op* ops, uint64_t* count)
 {
     return loc_pir_program_impl(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
-                                scratch_first, xor_tree, ops, count, false);
+                                scratch_first, xor_tree, ops, count, 0);
 }
 
 int locpir_b200_loc_pir_maj_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
@@ -906,7 +906,38 @@ int locpir_b200_loc_pir_maj_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t
                                     int xor_tree, locpir_b200_gate_op* ops, uint64_t* count)
 {
     return loc_pir_program_impl(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
-                                scratch_first, xor_tree, ops, count, true);
+                                scratch_first, xor_tree, ops, count, 1);
+}
+
+int locpir_b200_loc_pir_program_ex(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
+                                   const uint32_t* x_slots, const uint32_t* y_slots,
+                                   const uint32_t* bnd_slots, const int64_t* boxes,
+                                   const uint32_t* svc_slots, const uint32_t* out_slots,
+                                   uint64_t scratch_first, int xor_tree, int comparator,
+                                   locpir_b200_gate_op* ops, uint64_t* count)
+{
+    if (comparator < 0 || comparator > 2 || (!bnd_slots == !boxes))
+        return LOCPIR_B200_EINVAL;
+    if (bnd_slots)
+        return loc_pir_program_impl(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slots,
+                                    scratch_first, xor_tree, ops, count, comparator);
+    if (comparator == 1 || !count || !Q || !R || l < 2 || l > 63 || !m || !x_slots || !y_slots ||
+        !svc_slots || !out_slots || xor_tree < 0 || xor_tree > 2)
+        return LOCPIR_B200_EINVAL;
+    try {
+        std::vector<locpir_b200_gate_op> v;
+        emit_loc_pir_folded(v, Q, R, l, m, x_slots, y_slots, boxes, svc_slots, out_slots,
+                            scratch_first, xor_tree, comparator == 2);
+        if (ops) {
+            if (*count < v.size())
+                return LOCPIR_B200_EINVAL;
+            std::copy(v.begin(), v.end(), ops);
+        }
+        *count = v.size();
+        return LOCPIR_B200_OK;
+    } catch (...) {
+        return LOCPIR_B200_EINVAL;
+    }
 }
 
 uint64_t locpir_b200_loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)

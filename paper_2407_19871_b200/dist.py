@@ -145,7 +145,7 @@ class ShardedLocPir:
     evaluates its query shard against all boxes; outputs are gathered to rank 0.
     Every rank holds the same seeded batch `b` (inputs are encrypted deterministically)."""
 
-    def __init__(self, backend, b, rank, world, mode, seed, folded=False, maj=False):
+    def __init__(self, backend, b, rank, world, mode, seed, folded=False, maj=False, tree=False):
         from . import workloads as W
         self.be, self.b, self.rank, self.world, self.mode = backend, b, rank, world, mode
         Q, R, m = b.Q, b.R, b.m
@@ -155,12 +155,12 @@ class ShardedLocPir:
             self.G = sum(1 for lo, hi in self.spans if hi > lo)
             lo, hi = self.spans[rank]
             self.sub = W.sub_batch(b, 0, Q, lo, hi) if hi > lo else None
-            tree = 2 if world > 1 else 1
+            xor_mode = 2 if world > 1 else 1
         elif mode == "queries":
             self.spans = [shard_range(Q, r, world) for r in range(world)]
             lo, hi = self.spans[rank]
             self.sub = W.sub_batch(b, lo, hi, 0, R) if hi > lo else None
-            tree = 1
+            xor_mode = 1
         else:
             raise ValueError("mode must be 'boxes' or 'queries'")
         total = 0
@@ -176,7 +176,7 @@ class ShardedLocPir:
         backend.reserve(total)
         if self.sub is not None:
             backend.load(self.sub, self.lay, seed)
-            self.prog = backend.program(W.program_ops(self.sub, self.lay, tree, folded, maj))
+            self.prog = backend.program(W.program_ops(self.sub, self.lay, xor_mode, folded, maj, tree))
         if rank == 0 and mode == "boxes" and world > 1:
             self.combine = backend.program(W.combine_ops(self.G, Q, m, self.part_first,
                                                          self.out_first, self.comb_first))

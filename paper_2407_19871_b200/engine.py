@@ -409,6 +409,30 @@ def loc_pir_program(Q, R, l, m, x_slots, y_slots, bnd_slots, svc_slots, out_slot
     return ops
 
 
+COMPARATORS = {"reference": 0, "maj": 1, "tree": 2}
+
+
+def loc_pir_program_ex(Q, R, l, m, x_slots, y_slots, svc_slots, out_slots, scratch_first,
+                       bnd_slots=None, boxes_signed=None, xor_tree=True, comparator="reference"):
+    """locpir_b200_loc_pir_program_ex: boundaries as pool slots (bnd_slots) or plaintext
+    (boxes_signed, folded); comparator "reference" | "maj" | "tree" (flagged modes)."""
+    if (bnd_slots is None) == (boxes_signed is None):
+        raise ValueError("give exactly one of bnd_slots / boxes_signed")
+    arrs = [np.ascontiguousarray(v, np.uint32).reshape(-1)
+            for v in (x_slots, y_slots, svc_slots, out_slots)]
+    bnd = None if bnd_slots is None else np.ascontiguousarray(bnd_slots, np.uint32).reshape(-1)
+    bx = None if boxes_signed is None else np.ascontiguousarray(boxes_signed, np.int64).reshape(-1)
+    args = (Q, R, l, m, _u32(arrs[0]), _u32(arrs[1]), _u32(bnd) if bnd is not None else None,
+            bx.ctypes.data_as(C.POINTER(C.c_int64)) if bx is not None else None,
+            _u32(arrs[2]), _u32(arrs[3]), scratch_first, _tree_mode(xor_tree),
+            COMPARATORS[comparator])
+    cnt = C.c_uint64(0)
+    _check(lib().locpir_b200_loc_pir_program_ex(*args, None, C.byref(cnt)))
+    ops = (GateOp * cnt.value)()
+    _check(lib().locpir_b200_loc_pir_program_ex(*args, ops, C.byref(cnt)))
+    return ops
+
+
 def loc_pir_folded_program(Q, R, l, m, x_slots, y_slots, boxes_signed, svc_slots, out_slots,
                            scratch_first, xor_tree=True):
     """Flagged mode: loc_pir against PLAINTEXT box boundaries

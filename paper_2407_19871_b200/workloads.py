@@ -114,22 +114,29 @@ def signed_boxes(b: LocPirBatch) -> np.ndarray:
     return b.boxes.astype(np.int64) - (1 << (b.l - 1))
 
 
-def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False):
-    """folded=True: flagged plaintext-boundary mode; not for cfg5,
-    whose boundaries are encrypted.  maj=True: flagged majority-borrow comparators (any
-    boundaries)."""
-    from .engine import loc_pir_folded_program, loc_pir_program
+def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False,
+                tree=False):
+    """The batch's loc_pir gate program.  Flagged modes (not the reference gate count):
+    folded=True -- plaintext-boundary constant folding (plaintext boundaries
+    only); maj=True -- majority-borrow comparators; tree=True -- log-depth comparators
+    (latency mode)."""
+    from .engine import loc_pir_program_ex
+    if folded and b.encrypted_bounds:
+        raise ValueError("constant folding needs plaintext boundaries")
+    if folded and maj:
+        raise ValueError("the majority comparator works on boundary slots, not folded ones")
+    cmp = "tree" if tree else "maj" if maj else "reference"
     if folded:
-        if b.encrypted_bounds:
-            raise ValueError("constant folding needs plaintext boundaries")
-        return loc_pir_folded_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, signed_boxes(b),
-                                      lay.svc, lay.out, lay.scratch, xor_tree)
-    return loc_pir_program(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.bnd, lay.svc, lay.out,
-                           lay.scratch, xor_tree, maj)
+        return loc_pir_program_ex(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.svc, lay.out,
+                                  lay.scratch, boxes_signed=signed_boxes(b), xor_tree=xor_tree,
+                                  comparator=cmp)
+    return loc_pir_program_ex(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.svc, lay.out, lay.scratch,
+                              bnd_slots=lay.bnd, xor_tree=xor_tree, comparator=cmp)
 
 
-def program(ctx, b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False):
-    return ctx.program(program_ops(b, lay, xor_tree, folded, maj))
+def program(ctx, b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False,
+            tree=False):
+    return ctx.program(program_ops(b, lay, xor_tree, folded, maj, tree))
 
 
 def read_results(ctx, keys, b: LocPirBatch, lay: PoolLayout) -> np.ndarray:

@@ -10,7 +10,7 @@ import numpy as np  # noqa: E402
 from paper_2407_19871_b200 import ClientKeys, Context, TfheParams  # noqa: E402
 from paper_2407_19871_b200 import workloads as W  # noqa: E402
 
-for name in ("cfg1", "cfg1f"):
+for name in ("cfg1", "cfg1f", "cfg1t"):
     p = TfheParams(80)
     keys = ClientKeys(p, 20240719)
     ctx = Context(p, 0)
@@ -21,7 +21,7 @@ for name in ("cfg1", "cfg1f"):
     lay = W.PoolLayout(b)
     ctx.pool_reserve(lay.total)
     W.load_batch(ctx, keys, b, lay, seed=4)
-    prog = W.program(ctx, b, lay, folded=name.endswith("f"))
+    prog = W.program(ctx, b, lay, folded=name != "cfg1", tree=name.endswith("t"))
     prog.launch()
     ctx.sync()
     reps = 20
