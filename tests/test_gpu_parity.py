@@ -487,3 +487,26 @@ def test_pool_transfer_round_trip(dev, count, first):
     assert np.array_equal(back[first:first + count], rows)
     assert np.array_equal(back[:first], guard[:first])
     assert np.array_equal(back[first + count:], guard[first + count:])
+
+
+def test_empty_and_boundary_inputs(dev):
+    """Zero-count calls are no-ops, out-of-range slots and bad arguments fail loudly."""
+    from paper_2407_19871_b200 import _abi
+    from paper_2407_19871_b200.engine import InvalidArgument
+    p, keys, ctx = dev[128]
+    ctx.pool_reserve(64)
+    ctx.run([])                                               # empty program
+    ctx.load_queries([], 16, [], [])                          # no payloads
+    ctx.client_encrypt(keys.lwe_key, 1, np.zeros(0, np.uint32), first_slot=0)
+    assert ctx.store_responses([], 4) == []
+    with pytest.raises(InvalidArgument):                      # slot range past the pool
+        ctx.h2d(ctx.pool_capacity, keys.encrypt_bits(np.ones(1, np.uint8), 1))
+    with pytest.raises(InvalidArgument):
+        ctx.client_encrypt(np.full(p.n, 2, np.uint8), 1, np.zeros(1, np.uint32), 0)
+    with pytest.raises(InvalidArgument):
+        ctx.store_responses([ctx.pool_capacity - 1], 4)
+    with pytest.raises(InvalidArgument):                      # NOT of a never-written slot is fine,
+        ctx.run([(_abi.AND, 0, 1, _abi.SLOT_NONE, 0)])       # but writing a slot it reads is not
+    out = ctx.gate_batch_host(_abi.NAND, np.zeros((0, p.n + 1), np.uint32),
+                              np.zeros((0, p.n + 1), np.uint32))
+    assert out.shape == (0, p.n + 1)
