@@ -261,11 +261,11 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
     } else if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-        k_blind_rotate<3, 7><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
-                                                          c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
+        k_blind_rotate<3, 7><<<count, 64, BR_DYN_SMEM, c->stream>>>(
+            c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
     else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-        k_blind_rotate<2, 10><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
-                                                           c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
+        k_blind_rotate<2, 10><<<count, 64, BR_DYN_SMEM, c->stream>>>(
+            c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
     else
         throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
     CK(cudaGetLastError());
@@ -504,6 +504,12 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             for (int q = 0; q < 8; q++)
                 twq[q] = TW[64 * q];
             CK(cudaMemcpyToSymbol(c_twq, twq, sizeof(twq)));
+        }
+        if (BR_DYN_SMEM) {
+            CK(cudaFuncSetAttribute(k_blind_rotate<3, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)BR_DYN_SMEM));
+            CK(cudaFuncSetAttribute(k_blind_rotate<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)BR_DYN_SMEM));
         }
         CK(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(KS_CT * p->N * sizeof(uint16_t))));

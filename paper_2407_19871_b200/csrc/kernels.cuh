@@ -212,6 +212,46 @@ __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
 
 __constant__ double2 c_twq[8];  // psi^(64 q), q = 0..7 (TWIST_CONST)
 
+#ifndef BK_TMA
+#define BK_TMA 0
+#endif
+constexpr size_t BR_DYN_SMEM = BK_TMA ? 2 * FFT_M * sizeof(double2) : 0;
+// BK_TMA (opt-in): each CTA streams its BK rows with bulk async copies (TMA engine) into
+// a 16 KB shared-memory row buffer, completion tracked by an mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], pol;\n\t}\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
 template <int L, int BGBIT>
 __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     k_blind_rotate(DevParams dp, const BrItem* __restrict__ items,
@@ -232,6 +272,10 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
+#if BK_TMA
+    extern __shared__ __align__(128) double2 bkrow[];  // [2][FFT_M]: one BK row, both outputs
+    __shared__ __align__(8) uint64_t bkbar;
+#endif
 #if TWIST_TMEM
     if (t < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(
@@ -296,6 +340,39 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     auto bar = [] { __syncthreads(); };
     auto wbar = [] { __syncwarp(); };
     int xs = 0;  // alternating cross-warp tile
+#if BK_TMA
+    constexpr uint32_t ROW_BYTES = 2 * FFT_M * sizeof(double2);
+    // the row consumed next: (step, row) -- steps with abar = 0 are skipped
+    auto issue_row = [&](uint32_t step, int row) {
+        while (step < n && abar[step] == 0)
+            step++;
+        if (step < n)
+            tma_load_row(bkrow, bkf + ((size_t)step * (2 * L) + row) * 2 * FFT_M, ROW_BYTES, &bkbar);
+    };
+    uint32_t bkphase = 0;
+    if (t == 0)
+        mbar_init(&bkbar, 1);
+    __syncthreads();
+    if (t == 0)
+        issue_row(0, 0);
+#if BK_TMA == 2
+    // refill issued at the next transform's first CTA barrier (no extra barrier)
+    uint32_t pend_step = 0xFFFFFFFFu;
+    int pend_row = 0;
+    auto bar_tma = [&] {
+        __syncthreads();
+        if (t == 0 && pend_step != 0xFFFFFFFFu) {
+            issue_row(pend_step, pend_row);
+            pend_step = 0xFFFFFFFFu;
+        }
+    };
+#endif
+#endif
+#if BK_TMA == 2
+#define FFT_BAR bar_tma
+#else
+#define FFT_BAR bar
+#endif
 
     constexpr uint32_t HALF = 1u << (BGBIT - 1);
     constexpr uint32_t MASK = (1u << BGBIT) - 1;
@@ -331,17 +408,20 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             for (int p = 0; p < L; p++) {
                 // prefetch this row's BK slots; the loads land while the FFT runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
+#if !BK_TMA
                 double2 BA[8], BB[8];
-#if BK_PREFETCH >= 1
+#endif
+#if !BK_TMA && BK_PREFETCH >= 1
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BA[q] = ld_stream(row + q * 64 + t);
 #endif
-#if BK_PREFETCH >= 2
+#if !BK_TMA && BK_PREFETCH >= 2
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
 #endif
+                (void)row;
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
 #if TWIST_TMEM
@@ -358,8 +438,33 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 #if TWIST_TMEM
 #undef TWIST
 #endif
-                fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+                fft_forward(x, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
                 xs ^= 1;
+#if BK_TMA
+                mbar_wait(&bkbar, bkphase);
+                bkphase ^= 1u;
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    mac(oA[q], x[q], bkrow[q * 64 + t]);
+                    mac(oB[q], x[q], bkrow[FFT_M + q * 64 + t]);
+                }
+#if BK_TMA == 2
+                if (t == 0) {  // refill at the next CTA barrier (every thread is past this MAC)
+                    const int rw = c * L + p;
+                    pend_step = rw + 1 < 2 * L ? i : i + 1;
+                    pend_row = rw + 1 < 2 * L ? rw + 1 : 0;
+                }
+#else
+                __syncthreads();  // row buffer free: refill it with the next row
+                if (t == 0) {
+                    const int rw = c * L + p;
+                    if (rw + 1 < 2 * L)
+                        issue_row(i, rw + 1);
+                    else
+                        issue_row(i + 1, 0);
+                }
+#endif
+#else
 #if BK_PREFETCH < 2
 #pragma unroll
                 for (int q = 0; q < 8; q++)
@@ -375,10 +480,11 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                     mac(oA[q], x[q], BA[q]);
                     mac(oB[q], x[q], BB[q]);
                 }
+#endif
             }
         }
         // inverse transforms, round, accumulate into ACC
-        fft_inverse(oA, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+        fft_inverse(oA, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
         xs ^= 1;
 #if TWIST_TMEM
         uint32_t tv[32];
@@ -392,7 +498,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[0][j] += (uint32_t)__double2ll_rn(w.x);
             acc[0][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
-        fft_inverse(oB, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+        fft_inverse(oB, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
         xs ^= 1;
 #if TWIST_TMEM
         tmem_ld32(ttw, tv);
@@ -409,6 +515,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 #endif
     }
     __syncthreads();
+#undef FFT_BAR
     // ---- sample extraction at index 0 (N-dim LWE under the TRLWE key)
     uint32_t* o = pool_N + (size_t)it.out * dp.N_stride;
     for (int j = t; j < 1024; j += 64)
