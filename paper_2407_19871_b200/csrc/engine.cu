@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "br_warp.cuh"
 #include "br_pair.cuh"
+#include "br_lat2.cuh"
 #include "program.hpp"
 
 using namespace lpb;
@@ -124,6 +125,7 @@ struct locpir_b200_ctx {
     int br_pair = 0;  // LOCPIR_B200_BR=pair: paired digit transforms (k_blind_rotate_pair)
     // small levels (fewer bootstraps than SMs) take the latency kernels
     int small_levels = 1;
+    int lat_cluster = 0;  // LOCPIR_B200_LAT=cluster: 2-CTA cluster latency kernel (K1c)
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
     DevBuf<uint32_t> ks_partial;
     DevBuf<uint32_t> h2d_stage;  // packed rows for 1-D host copies (k_repack_rows)
@@ -232,7 +234,16 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
         return;
     timed_begin(c, 0);
     const uint32_t mu = 0x20000000u;
-    if (!c->br_warp && c->small_levels && count <= (uint32_t)c->num_sms) {
+    if (!c->br_warp && c->small_levels && c->lat_cluster && 2 * count <= (uint32_t)c->num_sms) {
+        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+            k_blind_rotate_lat2<3, 7><<<2 * count, 64 * 3, sizeof(Lat2Smem<3>), c->stream>>>(
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+            k_blind_rotate_lat2<2, 10><<<2 * count, 64 * 2, sizeof(Lat2Smem<2>), c->stream>>>(
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+        else
+            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    } else if (!c->br_warp && c->small_levels && count <= (uint32_t)c->num_sms) {
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
             k_blind_rotate_lat<3, 7><<<count, 128 * 3, sizeof(LatSmem<3>), c->stream>>>(
                 c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
@@ -517,6 +528,10 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
                                 (int)W_SMEM));
         CK(cudaFuncSetAttribute(k_blind_rotate_w<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)W_SMEM));
+        CK(cudaFuncSetAttribute(k_blind_rotate_lat2<3, 7>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Lat2Smem<3>)));
+        CK(cudaFuncSetAttribute(k_blind_rotate_lat2<2, 10>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Lat2Smem<2>)));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<3, 7>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<3>)));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<2, 10>,
@@ -525,6 +540,8 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             c->l2_persist = strcmp(lp, "0") != 0;
         if (const char* sl = getenv("LOCPIR_B200_SMALL"))
             c->small_levels = strcmp(sl, "0") != 0;
+        if (const char* lt = getenv("LOCPIR_B200_LAT"))
+            c->lat_cluster = strcmp(lt, "cluster") == 0;
         CK(cudaFuncSetAttribute(k_blind_rotate_pair<3, 7>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem)));
         CK(cudaFuncSetAttribute(k_blind_rotate_pair<2, 10>,
