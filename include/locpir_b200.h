@@ -17,8 +17,10 @@
  * Layouts.  An LWE sample is n+1 little-endian u32 words, mask then body --
  * exactly the reference wire layout (torus.hpp:226-237).  Host buffers are
  * [count][n+1]; device slots are padded to a 16-byte multiple internally.
- * Threading: one context per GPU; a context is not thread-safe (as a
- * GateEngine, gate_engine.hpp:335).  Execution is deterministic (no device RNG).
+ * Threading: one context per GPU; a context (and a server built on it) is not
+ * thread-safe (as a GateEngine, gate_engine.hpp:335).  Execution is deterministic:
+ * the only device randomness, locpir_b200_client_encrypt, is a counter-based stream
+ * (a pure function of key, seed and stream index).
  */
 #ifndef LOCPIR_B200_H
 #define LOCPIR_B200_H
