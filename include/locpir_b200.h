@@ -196,6 +196,11 @@ int locpir_b200_loc_pir_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
 int locpir_b200_debug_blind_rotate(locpir_b200_ctx* ctx, const uint32_t* lwe_n, uint64_t count,
                                    uint32_t* out_N);
 /* key switch of N-dim LWEs (N+1 words each) -> n-dim (n+1 words each) */
+/* FFT rounding margin: blind-rotates count combined n-dim LWEs with a diagnostic build of
+ * the throughput kernel and returns max |w - rint(w)| over every inverse-transform output
+ * before rounding (the pre-KS coefficients are exact iff this stays below 1/2). */
+int locpir_b200_debug_fft_error(locpir_b200_ctx* ctx, const uint32_t* lwe_n, uint64_t count,
+                                double* max_err);
 int locpir_b200_debug_keyswitch(locpir_b200_ctx* ctx, const uint32_t* lwe_N, uint64_t count,
                                 uint32_t* out_n);
 

@@ -108,6 +108,8 @@ SIGNATURES = [
     ("locpir_b200_client_encrypt", C.c_int,
      [_ctx, _u8p, C.c_uint64, C.c_uint32, _u32p, C.c_uint64, C.c_uint64]),
     ("locpir_b200_debug_blind_rotate", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
+    ("locpir_b200_debug_fft_error", C.c_int,
+     [_ctx, C.c_void_p, C.c_uint64, C.POINTER(C.c_double)]),
     ("locpir_b200_debug_keyswitch", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_void_p]),
     ("locpir_b200_timing_enable", C.c_int, [_ctx, C.c_int]),
     ("locpir_b200_kernel_stats", C.c_int, [_ctx, C.POINTER(C.c_double), _u64p]),

@@ -1258,6 +1258,53 @@ int locpir_b200_client_encrypt(locpir_b200_ctx* c, const uint8_t* lwe_key, uint6
     });
 }
 
+int locpir_b200_debug_fft_error(locpir_b200_ctx* c, const uint32_t* lwe_n, uint64_t count,
+                                double* max_err)
+{
+    return guarded(c, [&] {
+        if (!max_err || (count && !lwe_n))
+            throw std::invalid_argument("null buffer");
+        need_keys(c);
+        CK(cudaSetDevice(c->device));
+        *max_err = 0.0;
+        if (!count)
+            return;
+        if (c->pool_slots < count) {
+            int rc = locpir_b200_pool_reserve(c, count);
+            if (rc)
+                throw CudaError(c->err);
+        }
+        pool_copy(c, 0, count, lwe_n, nullptr, cudaMemcpyHostToDevice, true);
+        std::vector<BrItem> items(count);
+        for (uint64_t g = 0; g < count; g++)
+            items[g] = {(uint32_t)g, SLOT_NONE, 1, 0, 0u, (uint32_t)g, SLOT_NONE, 0};
+        if (count > c->scratch_slots) {
+            c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
+            c->scratch_slots = c->pool_N.n / c->dp.N_stride;
+        }
+        DevBuf<BrItem> d;
+        DevBuf<unsigned long long> e;
+        d.reserve(count + 1, c->stream, false);
+        e.reserve(1, c->stream, false);
+        CK(cudaMemsetAsync(e.p, 0, sizeof(unsigned long long), c->stream));
+        CK(cudaMemcpyAsync(d.p, items.data(), count * sizeof(BrItem), cudaMemcpyHostToDevice, c->stream));
+        const uint32_t mu = 0x20000000u;
+        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+            k_blind_rotate<3, 7, true><<<(unsigned)count, 64, BR_DYN_SMEM, c->stream>>>(
+                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu, e.p);
+        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+            k_blind_rotate<2, 10, true><<<(unsigned)count, 64, BR_DYN_SMEM, c->stream>>>(
+                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu, e.p);
+        else
+            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+        CK(cudaGetLastError());
+        unsigned long long bits = 0;
+        CK(cudaMemcpyAsync(&bits, e.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        std::memcpy(max_err, &bits, sizeof bits);
+    });
+}
+
 int locpir_b200_timing_enable(locpir_b200_ctx* c, int on)
 {
     if (!c)

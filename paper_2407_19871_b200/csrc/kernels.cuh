@@ -252,13 +252,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
         : "memory");
 }
 
-template <int L, int BGBIT>
+// ERR = true (diagnostic instantiation only): also record max |w - rint(w)| over every
+// inverse-transform output before rounding -- the FFT rounding margin (exact iff < 1/2).
+template <int L, int BGBIT, bool ERR = false>
 __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     k_blind_rotate(DevParams dp, const BrItem* __restrict__ items,
                    const uint32_t* __restrict__ pool_n, uint32_t* __restrict__ pool_N,
                    const double2* __restrict__ bkf, const double2* __restrict__ W,
-                   const double2* __restrict__ TW, const double2* __restrict__ UT, uint32_t mu)
+                   const double2* __restrict__ TW, const double2* __restrict__ UT, uint32_t mu,
+                   unsigned long long* err_out = nullptr)
 {
+    double emax = 0.0;
     __shared__ uint32_t acc[2][1024];
     // exchange tiles: [0],[1] cross-warp (alternating), [2] intra-warp
     __shared__ __align__(16) double2 xbuf[3][XTILE];
@@ -495,6 +499,8 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
             const double2 w = cmul(oA[q], untwist(TWIST(q)));
+            if constexpr (ERR)
+                emax = fmax(emax, fmax(fabs(w.x - rint(w.x)), fabs(w.y - rint(w.y))));
             acc[0][j] += (uint32_t)__double2ll_rn(w.x);
             acc[0][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
@@ -507,6 +513,8 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
             const double2 w = cmul(oB[q], untwist(TWIST(q)));
+            if constexpr (ERR)
+                emax = fmax(emax, fmax(fabs(w.x - rint(w.x)), fabs(w.y - rint(w.y))));
             acc[1][j] += (uint32_t)__double2ll_rn(w.x);
             acc[1][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
@@ -522,6 +530,8 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         o[j] = j == 0 ? acc[0][0] : 0u - acc[0][1024 - j];
     if (t == 0)
         o[1024] = acc[1][0];
+    if constexpr (ERR)  // positive doubles order like their bit patterns
+        atomicMax(err_out, (unsigned long long)__double_as_longlong(emax));
 #if TWIST_TMEM
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();

@@ -318,6 +318,15 @@ class Context:
                                                      out.ctypes.data))
         return out
 
+    def debug_fft_error(self, lwe_n: np.ndarray) -> float:
+        """Max |w - rint(w)| over every inverse-transform output of these blind rotations
+        (diagnostic kernel instantiation): the FFT rounding margin, exact iff < 1/2."""
+        lwe_n = np.ascontiguousarray(lwe_n, np.uint32).reshape(-1, self.params.n + 1)
+        e = C.c_double()
+        self._c(lib().locpir_b200_debug_fft_error(self.h, lwe_n.ctypes.data, lwe_n.shape[0],
+                                                  C.byref(e)))
+        return e.value
+
     def debug_keyswitch(self, lwe_N: np.ndarray) -> np.ndarray:
         lwe_N = np.ascontiguousarray(lwe_N, np.uint32).reshape(-1, self.params.N + 1)
         out = np.zeros((lwe_N.shape[0], self.params.n + 1), np.uint32)

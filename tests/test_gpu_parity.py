@@ -510,3 +510,23 @@ def test_empty_and_boundary_inputs(dev):
     out = ctx.gate_batch_host(_abi.NAND, np.zeros((0, p.n + 1), np.uint32),
                               np.zeros((0, p.n + 1), np.uint32))
     assert out.shape == (0, p.n + 1)
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_fft_rounding_margin(dev, level):
+    """the pre-KS coefficients are exact iff every inverse-transform output
+    lies within 1/2 of an integer; measure the worst distance over 2,048 blind rotations
+    (uniform random inputs and real NAND inputs) and pin it far below 1/2."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[level]
+    rng = np.random.default_rng(level + 1)
+    lwe = rng.integers(0, 2 ** 32, (1024, p.n + 1), dtype=np.uint64).astype(np.uint32)
+    bits = rng.integers(0, 2, (2, 1024)).astype(np.uint8)
+    a, b = keys.encrypt_bits(bits[0], 3), keys.encrypt_bits(bits[1], 4)
+    gate = ((0x20000000 + (0 - a.astype(np.int64)) + (0 - b.astype(np.int64))) & 0xFFFFFFFF)
+    gate[:, :-1] = (0 - a[:, :-1].astype(np.int64) - b[:, :-1].astype(np.int64)) & 0xFFFFFFFF
+    e1 = ctx.debug_fft_error(lwe)
+    e2 = ctx.debug_fft_error(gate.astype(np.uint32))
+    print(f"FFT rounding margin ({level}-bit): uniform {e1:.3e}, NAND inputs {e2:.3e}")
+    # 128-bit (Bgbit 7): a wide margin; 80-bit (Bgbit 10, digits to +-512): narrower but < 1/2
+    assert 0.0 < max(e1, e2) < (0.25 if level == 80 else 1.0 / 16)
