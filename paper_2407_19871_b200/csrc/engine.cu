@@ -487,6 +487,11 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
 {
     if (!p || !out || !locpir_b200_bk_words(p))
         return LOCPIR_B200_EINVAL;
+    // the device kernels are built for n <= 636 (K2 column coverage, abar arrays) and the
+    // two gadget shapes of the BASELINE parameter sets
+    if (p->n > MAX_CTX_N || !((p->bk_l == 3 && p->bk_bgbit == 7) || (p->bk_l == 2 && p->bk_bgbit == 10)))
+        return LOCPIR_B200_EINVAL;
+    static_assert(KS_THREADS * KS_COLS >= ((MAX_CTX_N + 1 + 3) & ~3u), "K2 column coverage");
     *out = nullptr;
     auto c = std::make_unique<locpir_b200_ctx>();
     c->p = *p;

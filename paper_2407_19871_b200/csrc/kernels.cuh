@@ -87,7 +87,11 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
 // ---------------------------------------------------------------------------
 // K1: blind rotation + sample extraction, one 64-thread CTA per ciphertext.
 // ---------------------------------------------------------------------------
-constexpr int MAX_N = 1023;
+// Largest LWE dimension the device kernels are built for: K2 covers KS_THREADS x KS_COLS
+// = 640 output columns (n+1 padded to 4), ctx_create rejects n > 636; abar arrays hold
+// MAX_N + 1 entries.
+constexpr int MAX_N = 639;
+constexpr uint32_t MAX_CTX_N = 636;
 #ifndef TWIST_REGS
 #define TWIST_REGS 0
 #endif
@@ -153,6 +157,30 @@ __device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32]
 
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};\n"
+        :
+        : "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+          "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
+          "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
 __device__ __forceinline__ double2 unpack2(const uint32_t* v)
 {
     return make_double2(__hiloint2double((int)v[1], (int)v[0]), __hiloint2double((int)v[3], (int)v[2]));
@@ -200,6 +228,20 @@ __device__ __forceinline__ double2 ld_stream(const double2* p)
     return v;
 }
 
+#ifndef I2F_MAGIC
+#define I2F_MAGIC 0
+#endif
+// int -> double for |d| < 2^31: exact either way; the magic-number form trades the
+// conversion instruction for one integer op and one DADD.
+__device__ __forceinline__ double i2d(int d)
+{
+#if I2F_MAGIC
+    return __dsub_rn(__hiloint2double(0x43300000, (uint32_t)d ^ 0x80000000u), 4503601774854144.0);
+#else
+    return (double)d;
+#endif
+}
+
 __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
 {
     double re = __fma_rn(F.x, B.x, acc.x);
@@ -214,6 +256,11 @@ __constant__ double2 c_twq[8];  // psi^(64 q), q = 0..7 (TWIST_CONST)
 
 #ifndef BK_TMA
 #define BK_TMA 0
+#endif
+// ACC_TMEM (opt-in): frequency-domain accumulators in TMEM (64 columns per CTA) and BK
+// loaded at MAC time, to fit 168 registers = 6 CTAs (12 warps) per SM.
+#ifndef ACC_TMEM
+#define ACC_TMEM 0
 #endif
 constexpr size_t BR_DYN_SMEM = BK_TMA ? 2 * FFT_M * sizeof(double2) : 0;
 // BK_TMA (opt-in): each CTA streams its BK rows with bulk async copies (TMA engine) into
@@ -279,6 +326,18 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 #if BK_TMA
     extern __shared__ __align__(128) double2 bkrow[];  // [2][FFT_M]: one BK row, both outputs
     __shared__ __align__(8) uint64_t bkbar;
+#endif
+#if ACC_TMEM
+    __shared__ uint32_t acc_tslot;
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&acc_tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tacc = acc_tslot + ((uint32_t)(t & 32) << 16);  // this warp's lane quarter
 #endif
 #if TWIST_TMEM
     if (t < 32) {
@@ -392,12 +451,16 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         const uint32_t a = abar[i];
         if (a == 0)
             continue;
+#if ACC_TMEM
+        bool first = true;
+#else
         double2 oA[8], oB[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             oA[q] = make_double2(0.0, 0.0);
             oB[q] = make_double2(0.0, 0.0);
         }
+#endif
         const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
 #pragma unroll
         for (int c = 0; c < 2; c++) {
@@ -412,15 +475,15 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             for (int p = 0; p < L; p++) {
                 // prefetch this row's BK slots; the loads land while the FFT runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
-#if !BK_TMA
+#if !BK_TMA && !ACC_TMEM
                 double2 BA[8], BB[8];
 #endif
-#if !BK_TMA && BK_PREFETCH >= 1
+#if !BK_TMA && !ACC_TMEM && BK_PREFETCH >= 1
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BA[q] = ld_stream(row + q * 64 + t);
 #endif
-#if !BK_TMA && BK_PREFETCH >= 2
+#if !BK_TMA && !ACC_TMEM && BK_PREFETCH >= 2
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
@@ -437,14 +500,38 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 for (int q = 0; q < 8; q++) {
                     const int dlo = (int)((tmp[q] >> sh) & MASK) - (int)HALF;
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
-                    x[q] = cmul(make_double2((double)dlo, (double)dhi), TWIST(q));
+                    x[q] = cmul(make_double2(i2d(dlo), i2d(dhi)), TWIST(q));
                 }
 #if TWIST_TMEM
 #undef TWIST
 #endif
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
                 xs ^= 1;
-#if BK_TMA
+#if ACC_TMEM
+                // MAC into the TMEM accumulators, 4 slots at a time; BK loaded here
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    uint32_t va[16], vb[16];
+                    if (!first) {
+                        tmem_ld16(tacc + 16 * h, va);
+                        tmem_ld16(tacc + 32 + 16 * h, vb);
+                    }
+#pragma unroll
+                    for (int qq = 0; qq < 4; qq++) {
+                        const int q = 4 * h + qq;
+                        double2 oa = first ? make_double2(0.0, 0.0) : unpack2(va + 4 * qq);
+                        double2 ob = first ? make_double2(0.0, 0.0) : unpack2(vb + 4 * qq);
+                        mac(oa, x[q], ld_stream(row + q * 64 + t));
+                        mac(ob, x[q], ld_stream(row + FFT_M + q * 64 + t));
+                        pack2(va + 4 * qq, oa);
+                        pack2(vb + 4 * qq, ob);
+                    }
+                    tmem_st16(tacc + 16 * h, va);
+                    tmem_st16(tacc + 32 + 16 * h, vb);
+                }
+                tmem_wait_st();
+                first = false;
+#elif BK_TMA
                 mbar_wait(&bkbar, bkphase);
                 bkphase ^= 1u;
 #pragma unroll
@@ -488,6 +575,16 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             }
         }
         // inverse transforms, round, accumulate into ACC
+#if ACC_TMEM
+        double2 oA[8], oB[8];
+        {
+            uint32_t v[32];
+            tmem_ld32(tacc, v);
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                oA[q] = unpack2(v + 4 * q);
+        }
+#endif
         fft_inverse(oA, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
         xs ^= 1;
 #if TWIST_TMEM
@@ -504,6 +601,15 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[0][j] += (uint32_t)__double2ll_rn(w.x);
             acc[0][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
+#if ACC_TMEM
+        {
+            uint32_t v[32];
+            tmem_ld32(tacc + 32, v);
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                oB[q] = unpack2(v + 4 * q);
+        }
+#endif
         fft_inverse(oB, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
         xs ^= 1;
 #if TWIST_TMEM
@@ -532,6 +638,13 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         o[1024] = acc[1][0];
     if constexpr (ERR)  // positive doubles order like their bit patterns
         atomicMax(err_out, (unsigned long long)__double_as_longlong(emax));
+#if ACC_TMEM
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (t < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(acc_tslot));
+#endif
 #if TWIST_TMEM
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();

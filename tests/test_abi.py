@@ -162,3 +162,18 @@ def test_plan_wave_structure_random_programs():
         pl = plan(ops)
         assert pl["levels"] == max(depth.values())
         assert pl["blind_rotations"] == n_ops == pl["key_switches"]
+
+
+def test_ctx_rejects_parameters_the_kernels_are_not_built_for():
+    """ctx_create checks the parameter set before touching the GPU: n beyond the key
+    switch's 640-column coverage and gadget shapes without a kernel instantiation."""
+    import ctypes as C
+    from paper_2407_19871_b200 import _abi
+    L = _abi.lib()
+    for n, l, bg in ((700, 3, 7), (630, 4, 6)):
+        p = _abi.Params()
+        assert L.locpir_b200_params_default(128, C.byref(p)) == 0
+        p.n, p.bk_l, p.bk_bgbit = n, l, bg
+        h = C.c_void_p()
+        assert L.locpir_b200_ctx_create(C.byref(p), 0, None, C.byref(h)) == _abi.EINVAL
+        assert not h.value
