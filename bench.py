@@ -53,6 +53,16 @@ def committed_traffic(kernel="k_blind_rotate<3, 7>"):
         return None
 
 
+def locpir_roofline(sec, units_per_query, qps, n_gpus, peak_tflops):
+    """BASELINE.json: queries/s as a fraction of the bootstrap roofline, the slower of the
+    transform arithmetic at the FP64 peak (units x F_BR) and the key bytes at HBM bandwidth
+    (|BK_freq| + |KSK| once per GPU: ~19 us, never the binding term)."""
+    f_br = flop_per_br(630, 1, 3, 1024) if sec == 128 else flop_per_br(500, 1, 2, 1024)
+    roof_qps = n_gpus * peak_tflops * 1e12 / (units_per_query * f_br)
+    return {"bound": "fp64", "queries_per_s_roof": roof_qps, "frac": qps / roof_qps,
+            "flop_per_unit": f_br}
+
+
 def hbm_view(G, params, avg_br_ms):
     """K1 against the measured HBM roof: algorithmic and ncu-measured DRAM bytes per launch
     over the launch time (MEASURED_PEAKS.json hbm_gbs)."""
@@ -355,6 +365,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
     from paper_2407_19871_b200 import ClientKeys, Context, TfheParams, workloads as W
     from paper_2407_19871_b200.dist import GpuBackend, ShardedLocPir
     from paper_2407_19871_b200.engine import plan
+    fp64_peak = ctx128.fp64_peak_tflops()
     out = {}
     ctx80 = keys80 = None
     for name, (sec, Qfull, R, l, m, enc) in W.CONFIGS.items():
@@ -432,6 +443,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                 "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
                                                            "(per-query cost is batch-independent "
                                                            "once the GPU is saturated)",
+                "roofline": locpir_roofline(sec, units / Qb, qtot / (ms / 1e3), ws, fp64_peak),
             }
             run.close()
     out["cfg4_server"] = run_server_sample(ctx128, keys128, ws, max_over_ranks)
