@@ -179,12 +179,17 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+_ORACLE_KEYS = {}
+
+
 def cpu_oracle_rate(budget_s=12.0, threads=None, seed=KEY_SEED):
     """Oracle port of TFHE gate bootstrapping (oracle/tfhe_oracle.c, FP64-FFT mode) on
     all host threads, static block partition as parallel.hpp:15-52.  Bounded sample."""
     from oracle import oracle as O
     threads = threads or os.cpu_count() or 1
-    K = O.TfheKeys(SECURITY, seed)
+    K = _ORACLE_KEYS.get((SECURITY, seed))
+    if K is None:  # key generation is setup, not part of any timed sample
+        K = _ORACLE_KEYS[(SECURITY, seed)] = O.TfheKeys(SECURITY, seed)
     s = O.NoiseSampler(seed + 1, K.p.alpha_in)
     one_a = np.stack([K.encrypt(1, s)])
     one_b = np.stack([K.encrypt(1, s)])
