@@ -357,7 +357,7 @@ def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
 
 # ---------------------------------------------------------------------------
 LOCPIR_SAMPLES = {  # name: queries timed per rank (a bounded sample of the config's batch)
-    "cfg1": 1, "cfg3": 1, "cfg4": 256, "cfg5": 8,
+    "cfg1": 1, "cfg3": 1, "cfg4": 256, "cfg5": 32,
 }
 
 
