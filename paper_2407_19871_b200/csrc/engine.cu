@@ -126,6 +126,7 @@ struct locpir_b200_ctx {
     // small levels (fewer bootstraps than SMs) take the latency kernels
     int small_levels = 1;
     int lat_cluster = 0;  // LOCPIR_B200_LAT=cluster: 2-CTA cluster latency kernel (K1c)
+    int use_graphs = 1;   // LOCPIR_B200_GRAPH=0: programs launch without CUDA graphs
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
     DevBuf<uint32_t> ks_partial;
     DevBuf<uint32_t> h2d_stage;  // packed rows for 1-D host copies (k_repack_rows)
@@ -343,6 +344,15 @@ struct locpir_b200_program {
     DevBuf<LinItem> lin;
     std::vector<size_t> ob, ok, ol;  // per-wave offsets
     uint64_t kernels = 0;
+    // CUDA graph of the launch sequence, valid for the device buffers in `sig`
+    cudaGraphExec_t exec = nullptr;
+    std::vector<const void*> sig;
+    uint64_t launches = 0;
+    ~locpir_b200_program()
+    {
+        if (exec)
+            cudaGraphExecDestroy(exec);
+    }
 };
 
 namespace {
@@ -379,8 +389,18 @@ void program_upload(locpir_b200_ctx* c, locpir_b200_program* pr, BrItem* hb, KsI
         CK(cudaMemcpyAsync(dl.p, hl, ol * sizeof(LinItem), cudaMemcpyHostToDevice, c->stream));
 }
 
-void program_enqueue(locpir_b200_ctx* c, const locpir_b200_program* pr, const BrItem* db,
+void program_kernels(locpir_b200_ctx* c, const locpir_b200_program* pr, const BrItem* db,
                      const KsItem* dk, const LinItem* dl)
+{
+    const Plan& P = pr->plan;
+    for (uint32_t w = 0; w < P.waves(); w++) {
+        launch_lin(c, dl + pr->ol[w], (uint32_t)P.lin[w].size());
+        launch_br(c, db + pr->ob[w], (uint32_t)P.br[w].size());
+        launch_ks(c, dk + pr->ok[w], (uint32_t)P.ks[w].size());
+    }
+}
+
+void program_prepare(locpir_b200_ctx* c, const locpir_b200_program* pr)
 {
     const Plan& P = pr->plan;
     if (P.n_br)
@@ -389,13 +409,22 @@ void program_enqueue(locpir_b200_ctx* c, const locpir_b200_program* pr, const Br
         c->pool_N.reserve((size_t)P.scratch * c->dp.N_stride, c->stream, false);
         c->scratch_slots = c->pool_N.n / c->dp.N_stride;
     }
-    for (uint32_t w = 0; w < P.waves(); w++) {
-        launch_lin(c, dl + pr->ol[w], (uint32_t)P.lin[w].size());
-        launch_br(c, db + pr->ob[w], (uint32_t)P.br[w].size());
-        launch_ks(c, dk + pr->ok[w], (uint32_t)P.ks[w].size());
-    }
+}
+
+void program_enqueue(locpir_b200_ctx* c, const locpir_b200_program* pr, const BrItem* db,
+                     const KsItem* dk, const LinItem* dl)
+{
+    program_prepare(c, pr);
+    program_kernels(c, pr, db, dk, dl);
     for (int i = 0; i < 9; i++)
-        c->counters[i] += P.counts[i];
+        c->counters[i] += pr->plan.counts[i];
+}
+
+// Every device pointer a captured launch sequence bakes in.
+std::vector<const void*> graph_signature(const locpir_b200_ctx* c)
+{
+    return {c->pool_n.p, c->pool_N.p, c->ks_partial.p, c->bkf.p, c->ksk.p,
+            c->W.p,      c->TW.p,     c->UT.p,         (const void*)c->stream};
 }
 
 size_t plan_items(const Plan& P, size_t& nb, size_t& nk, size_t& nl)
@@ -547,6 +576,8 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             c->small_levels = strcmp(sl, "0") != 0;
         if (const char* lt = getenv("LOCPIR_B200_LAT"))
             c->lat_cluster = strcmp(lt, "cluster") == 0;
+        if (const char* gr = getenv("LOCPIR_B200_GRAPH"))
+            c->use_graphs = strcmp(gr, "0") != 0;
         CK(cudaFuncSetAttribute(k_blind_rotate_pair<3, 7>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem)));
         CK(cudaFuncSetAttribute(k_blind_rotate_pair<2, 10>,
@@ -745,7 +776,42 @@ int locpir_b200_program_launch(locpir_b200_ctx* c, locpir_b200_program* pr)
     return guarded(c, [&] {
         if (!pr)
             throw std::invalid_argument("null program");
-        program_enqueue(c, pr, pr->br.p, pr->ks.p, pr->lin.p);
+        // The first launch runs directly (it also sizes every buffer: no allocation may
+        // happen under capture); later launches replay a CUDA graph of the whole level
+        // sequence, re-captured whenever a device buffer moved.  Timing mode (per-kernel
+        // events) and LOCPIR_B200_GRAPH=0 launch directly.
+        if (!c->use_graphs || c->timing || pr->launches == 0 || pr->plan.waves() == 0) {
+            program_enqueue(c, pr, pr->br.p, pr->ks.p, pr->lin.p);
+            pr->launches++;
+            return;
+        }
+        program_prepare(c, pr);
+        const auto sig = graph_signature(c);
+        if (!pr->exec || pr->sig != sig) {
+            if (pr->exec) {
+                CK(cudaGraphExecDestroy(pr->exec));
+                pr->exec = nullptr;
+            }
+            cudaGraph_t graph = nullptr;
+            CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                program_kernels(c, pr, pr->br.p, pr->ks.p, pr->lin.p);
+            } catch (...) {
+                cudaStreamEndCapture(c->stream, &graph);
+                if (graph)
+                    cudaGraphDestroy(graph);
+                throw;
+            }
+            CK(cudaStreamEndCapture(c->stream, &graph));
+            const cudaError_t e = cudaGraphInstantiate(&pr->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            CK(e);
+            pr->sig = sig;
+        }
+        CK(cudaGraphLaunch(pr->exec, c->stream));
+        for (int i = 0; i < 9; i++)
+            c->counters[i] += pr->plan.counts[i];
+        pr->launches++;
     });
 }
 

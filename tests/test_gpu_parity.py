@@ -530,3 +530,25 @@ def test_fft_rounding_margin(dev, level):
     print(f"FFT rounding margin ({level}-bit): uniform {e1:.3e}, NAND inputs {e2:.3e}")
     # 128-bit (Bgbit 7): a wide margin; 80-bit (Bgbit 10, digits to +-512): narrower but < 1/2
     assert 0.0 < max(e1, e2) < (0.25 if level == 80 else 1.0 / 16)
+
+
+def test_program_graph_replay_survives_pool_growth(dev):
+    """program_launch replays a CUDA graph after the first launch; growing the pool moves
+    the device buffers, which must trigger a re-capture (stale pointers would corrupt)."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[128]
+    G = 300
+    ctx.pool_reserve(3 * G)
+    rng = np.random.default_rng(11)
+    A, B = rng.integers(0, 2, G).astype(np.uint8), rng.integers(0, 2, G).astype(np.uint8)
+    ctx.h2d(0, keys.encrypt_bits(A, 5))
+    ctx.h2d(G, keys.encrypt_bits(B, 6))
+    prog = ctx.program([(_abi.XOR, g, G + g, _abi.SLOT_NONE, 2 * G + g) for g in range(G)])
+    for rounds in range(3):                      # direct launch, then graph replays
+        prog.launch()
+        assert np.array_equal(keys.decrypt_bits(ctx.d2h(2 * G, G)), A ^ B)
+    ctx.pool_reserve(ctx.pool_capacity * 4)      # reallocates (and copies) the pool
+    ctx.h2d(2 * G, np.zeros((G, p.n + 1), np.uint32))
+    prog.launch()
+    assert np.array_equal(keys.decrypt_bits(ctx.d2h(2 * G, G)), A ^ B)
+    prog.close()
