@@ -552,3 +552,31 @@ def test_program_graph_replay_survives_pool_growth(dev):
     prog.launch()
     assert np.array_equal(keys.decrypt_bits(ctx.d2h(2 * G, G)), A ^ B)
     prog.close()
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_flagged_gate_forms_on_the_throughput_kernel(dev, level, okeys80, okeys128):
+    """MAJ (3-input prologue), ANDNY and ORNY with more bootstraps per level than SMs, so
+    the throughput kernel (not the latency kernel) runs them: bit-exact with the oracle."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[level]
+    ok = okeys80 if level == 80 else okeys128
+    G = 600
+    rng = np.random.default_rng(level + 7)
+    bits = rng.integers(0, 2, (3, G)).astype(np.uint8)
+    cts = [keys.encrypt_bits(bits[i], 70 + i) for i in range(3)]
+    ctx.pool_reserve(6 * G)
+    for i in range(3):
+        ctx.h2d(i * G, cts[i])
+    ops = [(_abi.MAJ, g, G + g, 2 * G + g, 3 * G + g) for g in range(G)]
+    ops += [(_abi.ANDNY, g, G + g, _abi.SLOT_NONE, 4 * G + g) for g in range(G)]
+    ops += [(_abi.ORNY, g, G + g, _abi.SLOT_NONE, 5 * G + g) for g in range(G)]
+    ctx.run(ops)
+    a, b, c = bits
+    for base, want, kind in ((3, (a.astype(int) + b + c >= 2), "maj"), (4, (1 - a) & b, "andny"),
+                             (5, (1 - a) | b, "orny")):
+        got = ctx.d2h(base * G, G)
+        assert list(keys.decrypt_bits(got)) == list(np.asarray(want, np.uint8)), kind
+        for g in (0, G - 1):
+            args = (cts[0][g], cts[1][g], cts[2][g]) if kind == "maj" else (cts[0][g], cts[1][g])
+            assert np.array_equal(got[g], ok.gate(kind, *args)), kind
