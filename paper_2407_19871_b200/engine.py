@@ -622,3 +622,7 @@ class GateEngine:
 
     def hom_mux(self, sel, a, b):
         return self._emit(_abi.MUX, self._bit(sel), self._bit(a), self._bit(b))
+
+    def hom_maj(self, a, b, c):
+        """3-input majority in one bootstrap (flagged; not in the reference gate set)."""
+        return self._emit(_abi.MAJ, self._bit(a), self._bit(b), self._bit(c))

@@ -580,3 +580,16 @@ def test_flagged_gate_forms_on_the_throughput_kernel(dev, level, okeys80, okeys1
         for g in (0, G - 1):
             args = (cts[0][g], cts[1][g], cts[2][g]) if kind == "maj" else (cts[0][g], cts[1][g])
             assert np.array_equal(got[g], ok.gate(kind, *args)), kind
+
+
+def test_python_mirror_majority_gate(dev):
+    """GateEngine.hom_maj (flagged 3-input majority) through the Python mirror."""
+    from paper_2407_19871_b200 import GateEngine
+    p, keys, ctx = dev[80]
+    eng = GateEngine(ctx, keys, seed=8)
+    eng._next_slot = 0
+    for a in (0, 1):
+        for b in (0, 1):
+            for c in (0, 1):
+                ca, cb, cc = eng.encrypt(bool(a)), eng.encrypt(bool(b)), eng.encrypt(bool(c))
+                assert eng.decrypt(eng.hom_maj(ca, cb, cc)) == (a + b + c >= 2)
