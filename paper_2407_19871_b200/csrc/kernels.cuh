@@ -112,6 +112,10 @@ constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 2
 #endif
+#ifndef BR_PUNROLL
+#define BR_PUNROLL 1
+#endif
+constexpr int kPUnroll = BR_PUNROLL;  // digit-row loop unrolling in K1
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4
 #endif
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 tmp[q] = rot_read(acc[c], a, j) - acc[c][j] + OFF;
                 tmp[8 + q] = rot_read(acc[c], a, j + 512) - acc[c][j + 512] + OFF;
             }
-#pragma unroll 1
+#pragma unroll kPUnroll
             for (int p = 0; p < L; p++) {
                 // prefetch this row's BK slots; the loads land while the FFT runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
