@@ -377,7 +377,7 @@ def _random_program(rng, n_inputs, n_ops, first_slot):
     """Random SSA gate DAG over n_inputs input slots; returns (ops, plaintext evaluator)."""
     from paper_2407_19871_b200 import _abi
     kinds = [_abi.AND, _abi.OR, _abi.XOR, _abi.XNOR, _abi.NAND, _abi.NOR, _abi.MUX, _abi.NOT,
-             _abi.COPY, _abi.CONST]
+             _abi.COPY, _abi.CONST, _abi.ANDNY, _abi.ORNY, _abi.MAJ]
     live = list(range(n_inputs))
     ops = []
     nxt = first_slot
@@ -397,10 +397,13 @@ def _eval_plain(ops, vals):
     v = dict(vals)
     f = {_abi.AND: lambda a, b: a & b, _abi.OR: lambda a, b: a | b, _abi.XOR: lambda a, b: a ^ b,
          _abi.XNOR: lambda a, b: 1 - (a ^ b), _abi.NAND: lambda a, b: 1 - (a & b),
-         _abi.NOR: lambda a, b: 1 - (a | b)}
+         _abi.NOR: lambda a, b: 1 - (a | b), _abi.ANDNY: lambda a, b: (1 - a) & b,
+         _abi.ORNY: lambda a, b: (1 - a) | b}
     for k, a, b, c, o in ops:
         if k in f:
             v[o] = f[k](v[a], v[b])
+        elif k == _abi.MAJ:
+            v[o] = 1 if v[a] + v[b] + v[c] >= 2 else 0
         elif k == _abi.MUX:
             v[o] = v[b] if v[a] else v[c]
         elif k == _abi.NOT:
@@ -412,15 +415,16 @@ def _eval_plain(ops, vals):
     return v
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
-def test_random_gate_programs_level_scheduled(dev, seed):
-    """The circuit scheduler (csrc/program.hpp) on random DAGs of every gate kind: decrypted
-    outputs equal plaintext evaluation; the plan's bootstrap count equals the reference
-    accounting (MUX = 2 units, free gates 0)."""
+@pytest.mark.parametrize("seed,level,n_in,n_ops", [(1, 80, 48, 400), (2, 80, 48, 400),
+                                                  (3, 80, 48, 400), (4, 128, 600, 4000)])
+def test_random_gate_programs_level_scheduled(dev, seed, level, n_in, n_ops):
+    """The circuit scheduler (csrc/program.hpp) on random DAGs of every gate kind (incl.
+    the flagged ANDNY / ORNY / MAJ): decrypted outputs equal plaintext evaluation; the
+    plan's bootstrap count equals the accounting (MUX = 2 units, free gates 0).  The wide
+    128-bit case puts > #SM bootstraps in a level (throughput kernel)."""
     from paper_2407_19871_b200 import _abi, plan
-    p, keys, ctx = dev[80]
+    p, keys, ctx = dev[level]
     rng = np.random.default_rng(seed)
-    n_in, n_ops = 48, 400
     ops = _random_program(rng, n_in, n_ops, n_in)
     bits = rng.integers(0, 2, n_in).astype(np.uint8)
     ctx.pool_reserve(n_in + n_ops)
