@@ -112,6 +112,9 @@ constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 2
 #endif
+#ifndef INV_PAIR
+#define INV_PAIR 1
+#endif
 #ifndef BR_PUNROLL
 #define BR_PUNROLL 1
 #endif
@@ -578,6 +581,25 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 #endif
             }
         }
+#if INV_PAIR && !ACC_TMEM && !TWIST_TMEM
+        // both inverse transforms in lockstep: shared barriers, twice the ILP.  Tiles:
+        // intra and cross exchanges alias xbuf[2] / xbuf[xs] (a CTA barrier separates them)
+        fft_inverse2(oA, oB, tw, xbuf[2], xbuf[xs], xbuf[2], xbuf[xs], t, FFT_BAR, wbar);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int j = t + 64 * q;
+            const double2 ut = untwist(TWIST(q));
+            const double2 wa = cmul(oA[q], ut);
+            const double2 wb = cmul(oB[q], ut);
+            if constexpr (ERR)
+                emax = fmax(emax, fmax(fmax(fabs(wa.x - rint(wa.x)), fabs(wa.y - rint(wa.y))),
+                                       fmax(fabs(wb.x - rint(wb.x)), fabs(wb.y - rint(wb.y)))));
+            acc[0][j] += (uint32_t)__double2ll_rn(wa.x);
+            acc[0][j + 512] += (uint32_t)__double2ll_rn(wa.y);
+            acc[1][j] += (uint32_t)__double2ll_rn(wb.x);
+            acc[1][j + 512] += (uint32_t)__double2ll_rn(wb.y);
+        }
+#else
         // inverse transforms, round, accumulate into ACC
 #if ACC_TMEM
         double2 oA[8], oB[8];
@@ -628,6 +650,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j] += (uint32_t)__double2ll_rn(w.x);
             acc[1][j + 512] += (uint32_t)__double2ll_rn(w.y);
         }
+#endif
 #if TWIST_TMEM
 #undef TWIST
 #endif
