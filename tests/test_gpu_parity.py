@@ -597,3 +597,38 @@ def test_python_mirror_majority_gate(dev):
             for c in (0, 1):
                 ca, cb, cc = eng.encrypt(bool(a)), eng.encrypt(bool(b)), eng.encrypt(bool(c))
                 assert eng.decrypt(eng.hom_maj(ca, cb, cc)) == (a + b + c >= 2)
+
+
+def test_eager_and_level_batched_evaluation_give_identical_ciphertexts(dev):
+    """acceptance.cpp:416-447 (worker invariance), restated for the level scheduler: the
+    same loc_pir on the same input ciphertexts, evaluated gate by gate (one bootstrap per
+    launch) and level-batched, yields bit-identical output ciphertexts."""
+    from paper_2407_19871_b200 import GateEngine
+    from paper_2407_19871_b200.circuits import (EncodedRegion, FixedPointFormat, PlainWord,
+                                                ServiceCiphertext, constant_word, loc_pir)
+    p, keys, ctx = dev[80]
+    fmt = FixedPointFormat(4, 2)
+    l = fmt.total_bits()
+    rng = np.random.default_rng(31)
+    qbits = rng.integers(0, 2, 2 * l).astype(np.uint8)
+    sbits = rng.integers(0, 2, 2 * 3).astype(np.uint8)
+    q_cts = keys.encrypt_bits(qbits, 41)
+    s_cts = keys.encrypt_bits(sbits, 42)
+    outs = []
+    for batched in (False, True):
+        eng = GateEngine(ctx, keys, seed=5)
+        eng._next_slot = 0
+        qb = eng.load(q_cts)
+        sb = eng.load(s_cts)
+        from paper_2407_19871_b200.circuits import CipherWord
+        x, y = CipherWord(qb[:l], fmt), CipherWord(qb[l:], fmt)
+        regions = []
+        for i, (x1, x2, y1, y2) in enumerate(((-8, 6, -8, 8), (-3, 9, -10, 2))):
+            w = [constant_word(PlainWord.from_integer(v, fmt), eng) for v in (x1, x2, y1, y2)]
+            regions.append(EncodedRegion(*w, ServiceCiphertext(sb[3 * i:3 * i + 3]), i))
+        if not batched:  # every gate runs as its own one-bootstrap launch
+            import contextlib
+            eng.batch = lambda: contextlib.nullcontext(eng)
+        out = loc_pir(x, y, regions, eng, tree=True)
+        outs.append(eng.samples(out.bits))
+    assert np.array_equal(outs[0], outs[1])
