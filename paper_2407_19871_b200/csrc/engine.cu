@@ -246,10 +246,10 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
     } else if (!c->br_warp && c->small_levels && count <= (uint32_t)c->num_sms) {
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-            k_blind_rotate_lat<3, 7><<<count, 128 * 3, sizeof(LatSmem<3>), c->stream>>>(
+            k_blind_rotate_lat<3, 7><<<count, 128 * 3, kLatSmemBytes<3>, c->stream>>>(
                 c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-            k_blind_rotate_lat<2, 10><<<count, 128 * 2, sizeof(LatSmem<2>), c->stream>>>(
+            k_blind_rotate_lat<2, 10><<<count, 128 * 2, kLatSmemBytes<2>, c->stream>>>(
                 c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
@@ -567,9 +567,9 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
         CK(cudaFuncSetAttribute(k_blind_rotate_lat2<2, 10>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Lat2Smem<2>)));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<3, 7>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<3>)));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLatSmemBytes<3>));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<2, 10>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LatSmem<2>)));
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLatSmemBytes<2>));
         if (const char* lp = getenv("LOCPIR_B200_L2PERSIST"))
             c->l2_persist = strcmp(lp, "0") != 0;
         if (const char* sl = getenv("LOCPIR_B200_SMALL"))

@@ -112,6 +112,9 @@ constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 2
 #endif
+#ifndef LAT_TMA
+#define LAT_TMA 0
+#endif
 #ifndef INV_PAIR
 #define INV_PAIR 1
 #endif
@@ -287,6 +290,22 @@ __device__ __forceinline__ void tma_load_row(void* dst, const void* src, uint32_
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+    asm volatile(
+        "{\n\t.reg .b64 pol;\n\t"
+        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], pol;\n\t}\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
     asm volatile(
         "{\n\t.reg .b64 pol;\n\t"
         "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
@@ -1051,6 +1070,17 @@ struct LatSmem {
     double2 tiles[2 * L][2][XTILE];       // per group: cross-warp tile, intra-warp tile
     uint16_t abar[MAX_N + 1];
 };
+// 80-bit (L = 2): the whole BK_i (64 KB) also fits, streamed one step ahead by TMA
+template <int L>
+struct LatSmemBk {
+    LatSmem<L> s;
+    __align__(128) double2 bk[2 * L][2][FFT_M];
+    __align__(8) uint64_t bar;
+};
+template <int L>
+constexpr bool kLatTma = LAT_TMA && L == 2;
+template <int L>
+constexpr size_t kLatSmemBytes = kLatTma<L> ? sizeof(LatSmemBk<L>) : sizeof(LatSmem<L>);
 
 __device__ __forceinline__ void group_bar(int id)
 {
@@ -1087,6 +1117,33 @@ __global__ void __launch_bounds__(128 * L, 1)
         }
     }
     __syncthreads();
+    constexpr int ROWS_ = 2 * L;
+    [[maybe_unused]] uint32_t bkphase = 0;
+    [[maybe_unused]] auto issue_bk = [&](uint32_t step) {
+        if constexpr (kLatTma<L>) {
+            LatSmemBk<L>& SB = *reinterpret_cast<LatSmemBk<L>*>(smem_l);
+            while (step < n && S.abar[step] == 0)
+                step++;
+            if (step < n) {
+                constexpr uint32_t BYTES = ROWS_ * 2 * FFT_M * sizeof(double2);
+                const double2* src = bkf + (size_t)step * ROWS_ * 2 * FFT_M;
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                mbar_expect_tx(&SB.bar, BYTES);
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    bulk_copy(&SB.bk[0][0][0] + (size_t)k * (BYTES / 64), src + (size_t)k * (BYTES / 64),
+                              BYTES / 4, &SB.bar);
+            }
+        }
+    };
+    if constexpr (kLatTma<L>) {
+        LatSmemBk<L>& SB = *reinterpret_cast<LatSmemBk<L>*>(smem_l);
+        if (threadIdx.x == 0)
+            mbar_init(&SB.bar, 1);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            issue_bk(0);
+    }
     {
         const uint32_t e = (2048u - S.abar[n]) & 2047u;
         for (int j = threadIdx.x; j < 1024; j += blockDim.x) {
@@ -1122,7 +1179,7 @@ __global__ void __launch_bounds__(128 * L, 1)
             continue;
         // this thread's BK values for its MAC slots, in flight during the transform
         double2 bkv[ROWS][P];
-        {
+        if constexpr (!kLatTma<L>) {
             const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M + (size_t)mcomp * FFT_M;
 #pragma unroll
             for (int r = 0; r < ROWS; r++)
@@ -1157,18 +1214,39 @@ __global__ void __launch_bounds__(128 * L, 1)
                 S.F[g][q * 64 + t] = x[q];
         }
         __syncthreads();
+        if constexpr (kLatTma<L>) {
+            LatSmemBk<L>& SB = *reinterpret_cast<LatSmemBk<L>*>(smem_l);
+            mbar_wait(&SB.bar, bkphase);
+            bkphase ^= 1u;
 #pragma unroll
-        for (int k = 0; k < P; k++) {
-            const int q = msub + L * k;
-            if (q < 8) {
-                double2 o = make_double2(0.0, 0.0);
+            for (int k = 0; k < P; k++) {
+                const int q = msub + L * k;
+                if (q < 8) {
+                    double2 o = make_double2(0.0, 0.0);
 #pragma unroll
-                for (int r = 0; r < ROWS; r++)
-                    mac(o, S.F[r][q * 64 + t], bkv[r][k]);
-                S.O[mcomp][q * 64 + t] = o;
+                    for (int r = 0; r < ROWS; r++)
+                        mac(o, S.F[r][q * 64 + t], SB.bk[r][mcomp][q * 64 + t]);
+                    S.O[mcomp][q * 64 + t] = o;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < P; k++) {
+                const int q = msub + L * k;
+                if (q < 8) {
+                    double2 o = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int r = 0; r < ROWS; r++)
+                        mac(o, S.F[r][q * 64 + t], bkv[r][k]);
+                    S.O[mcomp][q * 64 + t] = o;
+                }
             }
         }
         __syncthreads();
+        if constexpr (kLatTma<L>) {  // BK buffer free: stream the next step's BK
+            if (threadIdx.x == 0)
+                issue_bk(i + 1);
+        }
         // groups 0 / 1: inverse transform of output component g, ACC update
         if (g < 2) {
             const int comp = g;
