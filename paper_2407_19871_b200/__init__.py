@@ -11,8 +11,12 @@ from ._abi import lib as _lib
 _lib()  # fail loudly at import when the CUDA extension is absent
 
 from .engine import (ClientKeys, CipherBit, Context, GateEngine, InvalidArgument,  # noqa: E402
-                     LogicError, TfheParams, loc_pir_program, parse_engine_kind, plan)
-from . import circuits  # noqa: E402,F401
+                     LogicError, TfheParams, check_query_payload, loc_pir_folded_program,
+                     loc_pir_program, loc_pir_program_ex, parse_engine_kind, plan)
+from .server import BatchingServer  # noqa: E402
+from . import circuits, workloads  # noqa: E402,F401
 
 __all__ = ["ClientKeys", "CipherBit", "Context", "GateEngine", "InvalidArgument", "LogicError",
-           "TfheParams", "loc_pir_program", "parse_engine_kind", "plan", "circuits"]
+           "TfheParams", "BatchingServer", "check_query_payload", "loc_pir_program",
+           "loc_pir_program_ex", "loc_pir_folded_program", "parse_engine_kind", "plan",
+           "circuits", "workloads"]
