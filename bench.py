@@ -209,7 +209,11 @@ def cpu_oracle_rate(budget_s=12.0, threads=None, seed=KEY_SEED):
     ok = all(K.decrypt(out[i]) == 1 - (A[i] & B[i]) for i in range(0, count, max(1, count // 64)))
     return {"value": count / dt, "unit": "gates/s", "cores": threads, "kind": "port",
             "sample": f"{count} NAND gates (128-bit TFHE, FP64-FFT oracle port, "
-                      f"{threads} threads, {dt:.1f} s)", "correct": bool(ok)}
+                      f"{threads} threads, {dt:.1f} s, build {ORACLE_BUILD})",
+            "gates": count, "seconds": dt,
+            "ms_per_gate_per_core": 1e3 * dt * threads / count,
+            "tfhe11_ms_per_gate_per_core": 13.0,  # PAPER.md:78 (TFHE 1.1, one core)
+            "correct": bool(ok)}
 
 
 def host_cpu():
@@ -280,14 +284,22 @@ def run_reference(args):
     for _ in range(args.steps):
         vals.append(cpu_oracle_rate(budget_s=args.ref_budget, threads=threads))
     v = statistics.median([x["value"] for x in vals])
+    # one step = one bounded sample of the cfg2 batch (cpu_oracle_rate); ms_per_step is the
+    # measured time of the gates actually evaluated in a step, not an extrapolation
     line = {
         "impl": "reference", "metric": "bootstrapped gates/s (128-bit TFHE)", "value": v,
         "unit": "gates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * GATES_PER_GPU / v, "higher_is_better": True,
+        "ms_per_step": 1000.0 * statistics.median([x["seconds"] for x in vals]),
+        "gates_per_step": statistics.median([x["gates"] for x in vals]),
+        "step_note": "each step evaluates a bounded sample (gates_per_step) of the 65,536-gate "
+                     "cfg2 batch; value = gates / s over those samples",
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": v, "unit": "gates/s", "cores": threads, "kind": "port",
-                         "sample": vals[-1]["sample"] + f"; median of {args.steps} steps"},
+                         "sample": vals[-1]["sample"] + f"; median of {args.steps} steps",
+                         "ms_per_gate_per_core": vals[-1]["ms_per_gate_per_core"],
+                         "tfhe11_ms_per_gate_per_core": 13.0, "host_cpu": host_cpu()},
         "e2e": {"value": v, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "The reference contains no gate bootstrapping (TFHE 1.1 is absent from "
                 "/root/reference); the timed CPU path is the oracle port of the TFHE "
@@ -356,7 +368,7 @@ def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
 
 
 # ---------------------------------------------------------------------------
-LOCPIR_SAMPLES = {  # name: queries timed per rank (a bounded sample of the config's batch)
+LOCPIR_SAMPLES = {  # name: queries timed per rank for the flagged modes and --locpir sample
     "cfg1": 1, "cfg3": 1, "cfg4": 256, "cfg5": 32,
 }
 
@@ -383,20 +395,6 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
             ctx, keys = ctx80, keys80
         else:
             ctx, keys = ctx128, keys128
-        Q = min(Qfull, LOCPIR_SAMPLES[name])
-        # cfg1 replicas (independent queries per GPU); cfg3 boxes sharded
-        # (partial XOR roots all-gathered, rank-0 combine level); cfg4/cfg5 queries
-        # sharded, results gathered to rank 0.  Every rank builds the same seeded batch.
-        if name == "cfg1":
-            mode, Qb, bseed, world, rk, scaling = "queries", Q, KEY_SEED + 17 * rank, 1, 0, "replicas"
-        elif name == "cfg3":
-            mode, Qb, bseed, world, rk, scaling = "boxes", Q, KEY_SEED + 3, ws, rank, "strong"
-        else:
-            mode, Qb, bseed, world, rk, scaling = "queries", Q * ws, KEY_SEED + 4, ws, rank, "weak"
-        b = W.make_batch(Qb, R, l, m, seed=bseed, encrypted_bounds=enc)
-        for q in range(min(Qb, R)):  # some queries inside boxes
-            b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
-            b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
         be = GpuBackend(ctx, keys, torch.device("cuda", local))
         # flagged modes (not the reference count): "folded" = plaintext-boundary constant
         # folding (plaintext boundaries only), "maj" = majority-borrow
@@ -407,15 +405,54 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                    ([("_maj", False, True, False)] if name in ("cfg4", "cfg5") else []) + \
                    ([("_tree", True, False, True)] if name == "cfg1" else [])
         for suffix, folded, maj, tree in variants:
-            lay_full = W.PoolLayout(b)
-            ops_full = W.program_ops(b, lay_full, True, folded, maj, tree)
-            pl = plan(ops_full)
-            units = pl["blind_rotations"]
-            run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj,
-                                tree=tree)
-            run.launch()  # warm-up
+            # the reference circuit runs the config at its stated size (all Qfull queries
+            # inside the timed region); flagged modes run a labelled per-GPU sample
+            full = suffix == "" and args.locpir == "full"
+            Q = Qfull if full else min(Qfull, LOCPIR_SAMPLES[name])
+            # cfg1 replicas (independent queries per GPU); cfg3 boxes sharded
+            # (partial XOR roots all-gathered, rank-0 combine level); cfg4/cfg5 queries
+            # sharded, results gathered to rank 0 (the stated batch split over the ranks
+            # when full, Q queries per rank for a sample).  Every rank builds the same
+            # seeded batch.
+            if name == "cfg1":
+                mode, Qb, bseed, world, rk, scaling = "queries", Q, KEY_SEED + 17 * rank, 1, 0, "replicas"
+            elif name == "cfg3":
+                mode, Qb, bseed, world, rk, scaling = "boxes", Q, KEY_SEED + 3, ws, rank, "strong"
+            elif full:
+                mode, Qb, bseed, world, rk, scaling = "queries", Q, KEY_SEED + 4, ws, rank, "strong"
+            else:
+                mode, Qb, bseed, world, rk, scaling = "queries", Q * ws, KEY_SEED + 4, ws, rank, "weak"
+            b = W.make_batch(Qb, R, l, m, seed=bseed, encrypted_bounds=enc)
+            for q in range(min(Qb, R)):  # some queries inside boxes
+                b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+                b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+            units_ref = b.units()
+            if Qb > 64:  # per-query counts from a small batch of the same shape (planning
+                small = W.sub_batch(b, 0, 4, 0, R)  # is linear in queries for fixed boxes)
+                pl = plan(W.program_ops(small, W.PoolLayout(small), True, folded, maj, tree))
+                units = pl["blind_rotations"] // 4 * Qb
+            else:
+                pl = plan(W.program_ops(b, W.PoolLayout(b), True, folded, maj, tree))
+                units = pl["blind_rotations"]
+            if full and Qb > 64:
+                # warm-up on a small batch of the same shape (kernels, L2 window); the full
+                # program's single timed launch enqueues its kernels directly
+                wb = W.sub_batch(b, 0, min(Qb, 8 * world), 0, R)
+                warm = ShardedLocPir(be, wb, rk, world, mode, seed=5000)
+                warm.launch()
+                torch.cuda.synchronize()
+                warm.close()
+                run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj,
+                                    tree=tree)
+                reps = 1
+            else:
+                run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj,
+                                    tree=tree)
+                run.launch()  # warm-up
+                reps = 3 if units < 200000 else 1
             torch.cuda.synchronize()
-            reps = 3 if units < 200000 else 1
+            if ws > 1:
+                torch.distributed.barrier()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
@@ -656,7 +693,87 @@ def run_b200(args):
     return 0
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` (N > 1) started as a plain process: re-launch this command as N
+    ranks, one process per GPU, the way the driver does (torch.distributed.run, rendezvous
+    on 127.0.0.1).  NCCL_DEBUG=INFO keeps NCCL's communicator lines (nranks) in stderr."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def run_dry(args):
+    """--dry-run (no GPU needed): the multi-rank plumbing of the bench -- rank spawn, gloo
+    process group, query sharding of a small cfg4-shaped batch, the gather to rank 0,
+    barrier-bracketed timing and the max over ranks -- with the plaintext interpreter of
+    tests/plain_backend.py (test infrastructure) standing in for each rank's GPU."""
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from plain_backend import PlainBackend
+    from paper_2407_19871_b200 import workloads as W
+    from paper_2407_19871_b200.dist import ShardedLocPir, max_over_ranks
+    sec, _, R, l, m, _ = W.CONFIGS["cfg4"]
+    Q = 8 * ws
+    b = W.make_batch(Q, R, l, m, seed=KEY_SEED + 4)
+    for q in range(min(Q, R)):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    run = ShardedLocPir(PlainBackend(), b, rank, ws, "queries", seed=5)
+    for _ in range(args.warmup):
+        run.launch()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run.launch()
+    if ws > 1:
+        dist.barrier()
+    dt = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    res = run.results()
+    if rank == 0:
+        print(json.dumps({
+            "dry_run": True, "metric": "LocPIR queries/s (plaintext interpreter, plumbing only)",
+            "value": Q / dt, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "correct": bool(np.array_equal(res, b.truth())),
+            "config": {"workload": f"cfg4 shape, {Q} queries x {R} boxes, queries sharded",
+                       "backend": "gloo"}}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+ORACLE_BUILD = "x86-64-v3"
+
+
+def select_oracle_build():
+    """The CPU baseline uses the AVX-512 build of the oracle port when the host has it
+    (bit-identical results: -ffp-contract=off, no fast-math)."""
+    global ORACLE_BUILD
+    v4 = os.path.join(ROOT, "oracle", "build", "liboracle_v4.so")
+    try:
+        flags = open("/proc/cpuinfo").read()
+    except OSError:
+        flags = ""
+    if " avx512f" in flags and os.path.exists(v4) and "LOCPIR_ORACLE_LIB" not in os.environ:
+        os.environ["LOCPIR_ORACLE_LIB"] = v4
+        ORACLE_BUILD = "x86-64-v4 (AVX-512)"
+
+
 def main():
+    select_oracle_build()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -667,9 +784,21 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-locpir", action="store_true",
                     help="skip the LocPIR queries/s measurements (configs 0, 2, 3, 4)")
+    ap.add_argument("--locpir", default="full", choices=["full", "sample"],
+                    help="full: cfg4/cfg5 reference circuits at their stated sizes (default); "
+                         "sample: LOCPIR_SAMPLES queries per GPU (quick runs)")
     ap.add_argument("--gates", type=int, default=GATES_PER_GPU,
                     help="gates per GPU (default: the cfg2 size; smaller only for profiling)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank plumbing only (gloo, plaintext interpreter, no GPU)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ws}")
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -55,9 +55,10 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("LOCPIR_ORACLE_LIB", LIB_PATH)  # bench.py: the AVX-512 build
+        if not os.path.exists(path):
             build()
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         u32p = C.POINTER(C.c_uint32)
         u8p = C.POINTER(C.c_uint8)
         L.or_keyset_generate.argtypes = [C.POINTER(KeySet), C.POINTER(Params), C.c_uint64]

@@ -106,11 +106,29 @@ def gather_counts_to_root(local: "torch.Tensor", counts: list, rank: int, world:
 # over gloo.
 # ---------------------------------------------------------------------------
 class GpuBackend:
-    """The B200 engine behind the sharded flow: pool slots hold ciphertext rows."""
+    """The B200 engine behind the sharded flow: pool slots hold ciphertext rows.
 
-    def __init__(self, ctx, keys, device):
-        self.ctx, self.keys, self.device = ctx, keys, device
+    staging "device" (NCCL): exported rows are device tensors.  The library enqueues its
+    copies and programs on the context's stream while NCCL orders its work after torch's
+    current stream, so export() makes the current stream wait for the context stream
+    (an event) before the collective reads the tensor, and import_() makes the context
+    stream wait for the current stream before it reads what the collective wrote.
+    staging "host" (gloo, e.g. several ranks sharing one GPU in tests): rows go through
+    host memory with synchronous copies."""
+
+    def __init__(self, ctx, keys, device, staging: str = "device"):
+        if staging not in ("device", "host"):
+            raise ValueError("staging must be 'device' or 'host'")
+        self.ctx, self.keys, self.device, self.staging = ctx, keys, device, staging
         self.row_words = ctx.params.n + 1
+
+    def _ctx_stream(self):
+        import torch
+        h = self.ctx.stream
+        cur = torch.cuda.current_stream(self.device)
+        if h == cur.cuda_stream:
+            return None, cur
+        return torch.cuda.ExternalStream(h, device=self.device), cur
 
     def reserve(self, slots):
         self.ctx.pool_reserve(slots)
@@ -124,14 +142,34 @@ class GpuBackend:
 
     def export(self, first, count):
         import torch
+        if self.staging == "host":
+            rows = self.ctx.d2h(first, count) if count else np.zeros((0, self.row_words), np.uint32)
+            return torch.from_numpy(rows.view(np.int32).copy())
         t = torch.empty((count, self.row_words), dtype=torch.int32, device=self.device)
         if count:
             self.ctx.store_device(first, count, t.data_ptr())
+        ext, cur = self._ctx_stream()
+        if ext is not None:  # the collective (on `cur`) must see the finished copy
+            ev = torch.cuda.Event()
+            ev.record(ext)
+            cur.wait_event(ev)
         return t
 
     def import_(self, first, t):
-        if t.shape[0]:
-            self.ctx.load_device(first, t.shape[0], t.data_ptr())
+        if not t.shape[0]:
+            return
+        if self.staging == "host":
+            self.ctx.h2d(first, t.cpu().numpy().view(np.uint32))
+            return
+        import torch
+        ext, cur = self._ctx_stream()
+        if ext is not None:  # the context stream must see what the collective wrote
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            ext.wait_event(ev)
+        self.ctx.load_device(first, t.shape[0], t.data_ptr())
+        if ext is not None:  # keep `t` alive until the library's copy has read it
+            t.record_stream(ext)
 
     def read_values(self, first, Q, m):
         bits = self.keys.decrypt_bits(self.ctx.d2h(first, Q * m)).reshape(Q, m).astype(np.uint64)

@@ -1,0 +1,88 @@
+"""Multi-rank paths on real ciphertexts.
+
+* `bench.py --gpus 2 --dry-run` (CPU): the bench spawns its own ranks when started as a
+  plain process, shards, gathers and reports the max over ranks with n_gpus = 2.
+* world = 2 on the single leased B200 (-m gpu): two processes, each with its own context
+  on cuda:0, run dist.ShardedLocPir over gloo.  Ciphertexts go GpuBackend.export ->
+  all_gather -> import_ -> rank-0 combine level ("boxes", cfg3's sharding) or gather to
+  rank 0 ("queries", cfg4/cfg5's sharding); rank 0 decrypts and compares with the
+  plaintext truth.  Both staging modes run: host rows, and device tensors through
+  gloo's CUDA path (the event ordering NCCL relies on).  Ranks never wait on each
+  other inside a kernel: the collective is on the host."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_bench_spawns_ranks_dry_run():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--steps", "2", "--warmup", "1"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["correct"] and d["steps"] == 2
+
+
+def _gpu_worker(rank, world, port, outdir, mode, staging, sec, Q, R, l, m):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2407_19871_b200 import Context, TfheParams
+    from paper_2407_19871_b200 import workloads as W
+    from paper_2407_19871_b200.dist import GpuBackend, ShardedLocPir, broadcast_keys
+    torch.cuda.set_device(0)
+    p = TfheParams(sec)
+    keys, bk, ksk = broadcast_keys(p, seed=7, rank=rank)  # gloo: CPU tensors
+    stream = torch.cuda.Stream()
+    ctx = Context(p, 0, stream=stream.cuda_stream)  # the library's own stream != current
+    ctx.upload_keys(bk.numpy().view(np.uint32), ksk.numpy().view(np.uint32))
+    b = W.make_batch(Q, R, l, m, seed=321)
+    for q in range(min(Q, R)):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    be = GpuBackend(ctx, keys, torch.device("cuda", 0), staging=staging)
+    run = ShardedLocPir(be, b, rank, world, mode, seed=5000)
+    for _ in range(2):  # second launch replays the CUDA graphs
+        run.launch()
+        torch.cuda.synchronize()
+        got = run.results()
+        if rank == 0:
+            ok = np.array_equal(got, b.truth())
+            with open(os.path.join(outdir, "res.txt"), "a") as f:
+                f.write(f"{int(ok)}\n")
+    dist.barrier()
+    run.close()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,staging,sec,Q,R", [
+    ("boxes", "host", 80, 2, 5), ("queries", "host", 80, 5, 3),
+    ("boxes", "device", 128, 2, 4), ("queries", "device", 128, 3, 2)])
+def test_sharded_locpir_world2_on_gpu(tmp_path, mode, staging, sec, Q, R):
+    mp.start_processes(_gpu_worker, args=(2, _free_port(), str(tmp_path), mode, staging, sec,
+                                          Q, R, 6, 3),
+                       nprocs=2, join=True, start_method="spawn")
+    res = open(tmp_path / "res.txt").read().split()
+    assert res == ["1", "1"], res

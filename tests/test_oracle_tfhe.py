@@ -4,6 +4,9 @@ Parity of these internals against TFHE 1.1 is unpinned (the library is absent
 from /root/reference); they are anchored on the reference's gate-level
 behaviour (truth tables, gate_engine.hpp:196-269) and on internal consistency:
 the FP64-FFT external product must equal the exact mod-2^32 product."""
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 import numpy as np
 import pytest
 
@@ -92,3 +95,30 @@ def test_bootstrapped_gate_truth_tables(oracle, level, okeys80, okeys128):
     sel = K.encrypt(1, s)
     assert K.decrypt(K.gate("mux", sel, K.encrypt(0, s), K.encrypt(1, s))) == 0
     assert K.decrypt(K.gate("mux", K.encrypt(0, s), K.encrypt(0, s), K.encrypt(1, s))) == 1
+
+
+def _gate_digest(env_lib):
+    import hashlib
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); from oracle import oracle as O;"
+            "K = O.TfheKeys(128, 7); s = O.NoiseSampler(3, K.p.alpha_in);"
+            "a = np.stack([K.encrypt(i & 1, s) for i in range(6)]);"
+            "b = np.stack([K.encrypt((i >> 1) & 1, s) for i in range(6)]);"
+            "sys.stdout.write(K.gate_batch('nand', a, b, O.FFT, 2).tobytes().hex())") % ROOT
+    env = dict(os.environ)
+    env.pop("LOCPIR_ORACLE_LIB", None)
+    if env_lib:
+        env["LOCPIR_ORACLE_LIB"] = env_lib
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                       timeout=600, check=True)
+    return hashlib.sha256(r.stdout.encode()).hexdigest()
+
+
+def test_avx512_baseline_build_is_bit_identical():
+    """bench.py's CPU baseline loads the x86-64-v4 build when the host has AVX-512; it must
+    produce the same ciphertexts as the default build (-ffp-contract=off, no fast-math)."""
+    v4 = os.path.join(ROOT, "oracle", "build", "liboracle_v4.so")
+    if " avx512f" not in open("/proc/cpuinfo").read() or not os.path.exists(v4):
+        pytest.skip("no AVX-512 host or no v4 build")
+    assert _gate_digest(v4) == _gate_digest(None)
