@@ -371,6 +371,9 @@ def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
 LOCPIR_SAMPLES = {  # name: queries timed per rank for the flagged modes and --locpir sample
     "cfg1": 1, "cfg3": 1, "cfg4": 256, "cfg5": 32,
 }
+# queries per program at the stated sizes (each program's scratch: ~19.6 MB per cfg4 query,
+# ~154 MB per cfg5 query; every level still spans >= 10 waves of the 148 SMs)
+LOCPIR_CHUNK = {"cfg4": 512, "cfg5": 128}
 
 
 def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
@@ -435,15 +438,18 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                 pl = plan(W.program_ops(b, W.PoolLayout(b), True, folded, maj, tree))
                 units = pl["blind_rotations"]
             if full and Qb > 64:
-                # warm-up on a small batch of the same shape (kernels, L2 window); the full
-                # program's single timed launch enqueues its kernels directly
+                # stated size: programs of LOCPIR_CHUNK queries sharing one scratch region
+                # (every query inside the timed region); warm-up on a small batch of the
+                # same shape (kernels, L2 window), then scratch sized before timing -- the
+                # full programs' single timed launch enqueues their kernels directly
                 wb = W.sub_batch(b, 0, min(Qb, 8 * world), 0, R)
                 warm = ShardedLocPir(be, wb, rk, world, mode, seed=5000)
                 warm.launch()
                 torch.cuda.synchronize()
                 warm.close()
                 run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj,
-                                    tree=tree)
+                                    tree=tree, chunk=LOCPIR_CHUNK[name])
+                run.prepare()
                 reps = 1
             else:
                 run = ShardedLocPir(be, b, rk, world, mode, seed=5000, folded=folded, maj=maj,
@@ -482,6 +488,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                         ("flagged: majority-borrow comparators, N(4l+2m+3) units (not the "
                          "reference gate count)") if maj else
                         "reference circuit (N(12l+2m+3) units)",
+                "programs": len(run.progs),
                 "sample": "full config" if Q == Qfull else f"{Q} of {Qfull} queries per GPU "
                                                            "(per-query cost is batch-independent "
                                                            "once the GPU is saturated)",

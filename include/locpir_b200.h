@@ -143,6 +143,9 @@ typedef struct locpir_b200_program locpir_b200_program;
 int locpir_b200_program_create(locpir_b200_ctx* ctx, const locpir_b200_gate_op* ops,
                                uint64_t count, locpir_b200_program** out);
 int locpir_b200_program_launch(locpir_b200_ctx* ctx, locpir_b200_program* prog);
+/* Sizes the context's scratch for the program (and checks the keys are uploaded) so
+ * that its first launch allocates nothing; optional. */
+int locpir_b200_program_prepare(locpir_b200_ctx* ctx, locpir_b200_program* prog);
 /* kernel launches one program_launch issues */
 uint64_t locpir_b200_program_kernels(const locpir_b200_program* prog);
 void locpir_b200_program_destroy(locpir_b200_program* prog);

@@ -60,6 +60,7 @@ SIGNATURES = [
     ("locpir_b200_sync", C.c_int, [_ctx]),
     ("locpir_b200_program_create", C.c_int, [_ctx, _ops, C.c_uint64, C.POINTER(C.c_void_p)]),
     ("locpir_b200_program_launch", C.c_int, [_ctx, C.c_void_p]),
+    ("locpir_b200_program_prepare", C.c_int, [_ctx, C.c_void_p]),
     ("locpir_b200_program_kernels", C.c_uint64, [C.c_void_p]),
     ("locpir_b200_program_destroy", None, [C.c_void_p]),
     ("locpir_b200_plan", C.c_int, [_ops, C.c_uint64, _u32p, _u64p, _u64p]),

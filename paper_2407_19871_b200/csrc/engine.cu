@@ -815,6 +815,15 @@ int locpir_b200_program_launch(locpir_b200_ctx* c, locpir_b200_program* pr)
     });
 }
 
+int locpir_b200_program_prepare(locpir_b200_ctx* c, locpir_b200_program* pr)
+{
+    return guarded(c, [&] {
+        if (!pr)
+            throw std::invalid_argument("null program");
+        program_prepare(c, pr);  // keys present, N-dim scratch sized: no allocation at launch
+    });
+}
+
 uint64_t locpir_b200_program_kernels(const locpir_b200_program* pr) { return pr ? pr->kernels : 0; }
 
 void locpir_b200_program_destroy(locpir_b200_program* pr)

@@ -183,11 +183,16 @@ class ShardedLocPir:
     evaluates its query shard against all boxes; outputs are gathered to rank 0.
     Every rank holds the same seeded batch `b` (inputs are encrypted deterministically)."""
 
-    def __init__(self, backend, b, rank, world, mode, seed, folded=False, maj=False, tree=False):
+    def __init__(self, backend, b, rank, world, mode, seed, folded=False, maj=False, tree=False,
+                 chunk=None):
+        """chunk (mode "queries"): evaluate the rank's queries as programs of at most
+        `chunk` queries sharing one scratch region (workloads.PoolLayout), launched in
+        order on the context stream."""
         from . import workloads as W
         self.be, self.b, self.rank, self.world, self.mode = backend, b, rank, world, mode
         Q, R, m = b.Q, b.R, b.m
         self.prog = self.combine = None
+        self.progs = []
         if mode == "boxes":
             self.spans = [shard_range(R, r, world) for r in range(world)]
             self.G = sum(1 for lo, hi in self.spans if hi > lo)
@@ -203,7 +208,7 @@ class ShardedLocPir:
             raise ValueError("mode must be 'boxes' or 'queries'")
         total = 0
         if self.sub is not None:
-            self.lay = W.PoolLayout(self.sub)
+            self.lay = W.PoolLayout(self.sub, chunk if mode == "queries" else None)
             total = self.lay.total
         # rank-0 regions: gathered partials / outputs, final outputs, combine scratch
         self.part_first = total
@@ -214,7 +219,10 @@ class ShardedLocPir:
         backend.reserve(total)
         if self.sub is not None:
             backend.load(self.sub, self.lay, seed)
-            self.prog = backend.program(W.program_ops(self.sub, self.lay, xor_mode, folded, maj, tree))
+            self.progs = [backend.program(W.program_ops(self.sub, self.lay, xor_mode, folded, maj,
+                                                        tree, lo, hi))
+                          for lo, hi in self.lay.chunks()]
+            self.prog = self.progs[0]
         if rank == 0 and mode == "boxes" and world > 1:
             self.combine = backend.program(W.combine_ops(self.G, Q, m, self.part_first,
                                                          self.out_first, self.comb_first))
@@ -226,8 +234,8 @@ class ShardedLocPir:
         """Local program, then the exchange (all-gather / gather to rank 0) and, for box
         shards, rank 0's combine level."""
         import torch.distributed as dist
-        if self.prog is not None:
-            self.prog.launch()
+        for p in self.progs:
+            p.launch()
         if self.world == 1:
             return
         b = self.b
@@ -261,7 +269,12 @@ class ShardedLocPir:
         first = self.out_first if self.mode == "boxes" else self.part_first
         return self.be.read_values(first, b.Q, b.m)
 
+    def prepare(self):
+        """Size every program's scratch ahead of the first (timed) launch."""
+        for p in self.progs + ([self.combine] if self.combine is not None else []):
+            if hasattr(p, "prepare"):
+                p.prepare()
+
     def close(self):
-        for p in (self.prog, self.combine):
-            if p is not None:
-                p.close()
+        for p in self.progs + ([self.combine] if self.combine is not None else []):
+            p.close()

@@ -361,6 +361,11 @@ class Program:
     def launch(self):
         self.ctx._c(lib().locpir_b200_program_launch(self.ctx.h, self.h))
 
+    def prepare(self):
+        """Size the context's scratch for this program now (its first launch then
+        allocates nothing)."""
+        self.ctx._c(lib().locpir_b200_program_prepare(self.ctx.h, self.h))
+
     def close(self):
         if getattr(self, "h", None):
             lib().locpir_b200_program_destroy(self.h)

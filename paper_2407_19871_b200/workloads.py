@@ -75,10 +75,15 @@ def _bits_signed(u: np.ndarray, l: int) -> np.ndarray:
 
 
 class PoolLayout:
-    """Slot assignment for one batch in the device pool."""
+    """Slot assignment for one batch in the device pool.  chunk: the batch is evaluated
+    as programs of at most `chunk` queries that share one scratch region (launched one
+    after another on the context stream), so scratch is sized for a chunk, not the
+    batch -- every intermediate of a loc_pir program has its own slot, ~7.8K slots
+    (19.6 MB) per cfg4 query."""
 
-    def __init__(self, b: LocPirBatch):
+    def __init__(self, b: LocPirBatch, chunk: int | None = None):
         Q, R, l, m = b.Q, b.R, b.l, b.m
+        self.chunk = min(Q, chunk) if chunk else Q
         n = 0
         self.x = n + np.arange(Q * l, dtype=np.uint32).reshape(Q, l); n += Q * l
         self.y = n + np.arange(Q * l, dtype=np.uint32).reshape(Q, l); n += Q * l
@@ -88,8 +93,15 @@ class PoolLayout:
         self.scratch = n
         self.inputs_end = self.out.min()
         from ._abi import lib
-        self.total = n + max(lib().locpir_b200_loc_pir_scratch(Q, R, l, m),
-                             lib().locpir_b200_loc_pir_folded_scratch(Q, R, l, m))
+        Qc = max(1, self.chunk)
+        self.total = n + max(lib().locpir_b200_loc_pir_scratch(Qc, R, l, m),
+                             lib().locpir_b200_loc_pir_folded_scratch(Qc, R, l, m))
+
+    def chunks(self):
+        """[q_lo, q_hi) query ranges of the programs."""
+        Q = self.x.shape[0]
+        c = max(1, self.chunk)
+        return [(lo, min(Q, lo + c)) for lo in range(0, Q, c)] if Q else []
 
 
 def load_batch(ctx, keys, b: LocPirBatch, lay: PoolLayout, seed: int):
@@ -115,22 +127,25 @@ def signed_boxes(b: LocPirBatch) -> np.ndarray:
 
 
 def program_ops(b: LocPirBatch, lay: PoolLayout, xor_tree=True, folded=False, maj=False,
-                tree=False):
-    """The batch's loc_pir gate program.  Flagged modes (not the reference gate count):
-    folded=True -- plaintext-boundary constant folding (plaintext boundaries
-    only); maj=True -- majority-borrow comparators; tree=True -- log-depth comparators
-    (latency mode)."""
+                tree=False, q_lo: int = 0, q_hi: int | None = None):
+    """The loc_pir gate program of queries [q_lo, q_hi) of the batch (default: all).
+    Flagged modes (not the reference gate count): folded=True -- plaintext-boundary
+    constant folding (plaintext boundaries only); maj=True --
+    majority-borrow comparators; tree=True -- log-depth comparators (latency mode)."""
     from .engine import loc_pir_program_ex
     if folded and b.encrypted_bounds:
         raise ValueError("constant folding needs plaintext boundaries")
     if folded and maj:
         raise ValueError("the majority comparator works on boundary slots, not folded ones")
+    q_hi = b.Q if q_hi is None else q_hi
+    Q = q_hi - q_lo
+    x, y, out = lay.x[q_lo:q_hi], lay.y[q_lo:q_hi], lay.out[q_lo:q_hi]
     cmp = "tree" if tree else "maj" if maj else "reference"
     if folded:
-        return loc_pir_program_ex(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.svc, lay.out,
+        return loc_pir_program_ex(Q, b.R, b.l, b.m, x, y, lay.svc, out,
                                   lay.scratch, boxes_signed=signed_boxes(b), xor_tree=xor_tree,
                                   comparator=cmp)
-    return loc_pir_program_ex(b.Q, b.R, b.l, b.m, lay.x, lay.y, lay.svc, lay.out, lay.scratch,
+    return loc_pir_program_ex(Q, b.R, b.l, b.m, x, y, lay.svc, out, lay.scratch,
                               bnd_slots=lay.bnd, xor_tree=xor_tree, comparator=cmp)
 
 

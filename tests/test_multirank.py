@@ -117,3 +117,24 @@ def test_sharded_locpir_gloo(tmp_path, mode, world, Q, R):
     got = np.load(tmp_path / "got.npy")
     assert np.array_equal(got, np.load(tmp_path / "truth.npy"))
     assert int(np.load(tmp_path / "xors.npy")[0]) == Q * R * m
+
+
+def test_chunked_query_programs_match_truth():
+    """Query batches evaluated as several programs sharing one scratch region (the bench's
+    stated-size cfg4/cfg5 runs) give the same answers as one program."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from plain_backend import PlainBackend
+    from paper_2407_19871_b200 import workloads as W
+    from paper_2407_19871_b200.dist import ShardedLocPir
+    b = W.make_batch(7, 3, 8, 3, seed=99)
+    for q in range(3):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    one = ShardedLocPir(PlainBackend(), b, 0, 1, "queries", seed=5)
+    chunked = ShardedLocPir(PlainBackend(), b, 0, 1, "queries", seed=5, chunk=3)
+    assert len(chunked.progs) == 3 and len(one.progs) == 1
+    assert chunked.lay.total < one.lay.total
+    for r in (one, chunked):
+        r.launch()
+        assert np.array_equal(r.results(), b.truth())
