@@ -83,6 +83,8 @@ def lib():
         L.or_fft_tables.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.or_fft_forward_i32.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p]
         L.or_fft_inverse_add.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p]
+        L.or_fft_margin.argtypes = [C.c_int]
+        L.or_fft_margin.restype = C.c_double
         L.or_polymul_exact_add.argtypes = [C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.or_decompose.argtypes = [C.POINTER(Params), u32p, C.c_uint32, C.c_void_p]
         L.or_mod_switch.argtypes = [C.c_uint32, C.c_uint32]
@@ -193,6 +195,12 @@ def fft_forward(d: np.ndarray) -> np.ndarray:
 def fft_inverse_add(F: np.ndarray, acc: np.ndarray) -> None:
     F = np.array(F, np.float64, copy=True)
     lib().or_fft_inverse_add(len(acc), F.ctypes.data, acc.ctypes.data)
+
+
+def fft_margin(reset: bool = True) -> float:
+    """Max distance from an integer of any inverse-transform output before rounding since
+    the last reset (the FFT rounding margin; exact while < 1/2)."""
+    return lib().or_fft_margin(1 if reset else 0)
 
 
 def polymul_exact_add(d: np.ndarray, b: np.ndarray, acc: np.ndarray) -> None:

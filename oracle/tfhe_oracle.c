@@ -190,12 +190,34 @@ size_t or_ksk_words(const or_params* p)
 }
 
 /* ------------------------------------------------------------------------ */
-/* Negacyclic FP64 transform.                                                */
-/*   forward: z_j = (a_j + i a_{j+M}) * psi^j, psi = e^{i pi / N}, M = N/2;  */
-/*            radix-2 DIF over M points with W[k] = e^{+2 pi i k / M};       */
-/*            output in bit-reversed order.                                   */
-/*   inverse: radix-2 DIT with conj(W), then * conj(psi^j) / M, round.       */
-/* cmul(x, w) = (fma(xr, wr, -(xi*wi)), fma(xr, wi, xi*wr)).                 */
+/* Negacyclic FP64 transform (N = 1024 -> M = 512 complex points).           */
+/* This is the arithmetic contract the B200 kernels execute operation for     */
+/* operation (paper_2407_19871_b200/csrc/fft.cuh); TFHE's own FFT is absent   */
+/* from /root/reference (parity unpinned, anchored on FFT == exact product).  */
+/*                                                                            */
+/* forward: a_j = d_j + i d_{j+M} (integers).  Evaluates P(Y) = sum a_j Y^j   */
+/*   at the M roots of Y^M = i, i.e. Z_k = sum_j a_j psi^j W^{jk}             */
+/*   (psi = e^{i pi/N}, W = e^{2 pi i/M}): the negacyclic twist is absorbed   */
+/*   into the twiddles.  Cooley-Tukey recursion P mod (Y^{2h} - c) ->          */
+/*   P mod (Y^h -+ r), r^2 = c: butterfly (u, v) -> (u + r v, u - r v).        */
+/*   Tree node v = 2^s + b (stage s, block b) has modulus Y^{2h} - psi^E[v],   */
+/*   E[1] = N/2, children E[v]/2 and E[v]/2 + N (mod 2N); twiddle             */
+/*   r = psi^(E[v]/2).  Output slot b holds Z_{bitrev9(b)}.                   */
+/* inverse: plain inverse DFT, radix-2 DIT, bit-reversed in -> natural out,   */
+/*   twiddles conj(W^e), then the untwist conj(TW[j]) (TW = factored psi^j).  */
+/*   The 1/M scale is folded into the frequency-domain BK (exact).            */
+/*                                                                            */
+/* Butterfly forms (every op rounds once, no contraction beyond the fma()s):  */
+/*   CT(c, t):   w = c (1 + i t);  s = (fma(-vi, t, vr), fma(vr, t, vi));     */
+/*               u' = (fma(c, sr, ur), fma(c, si, ui));                       */
+/*               v' = (fma(-c, sr, ur), fma(-c, si, ui))        [6 fma]       */
+/*   a rotation v -> i v or -i v (exact) may precede it;                      */
+/*   STD(w):     t = cmul(v, w); u' = u + t; v' = u - t          [8 ops]      */
+/*   trivial:    w = 1 or w = -i                                 [4 adds]     */
+/* Which form each butterfly uses follows the GPU's 8 x 8 x 8 register layout */
+/* (three passes of three stages): a stage's twiddle is a per-thread register */
+/* value at the first stage of a pass and a register value times a compile-   */
+/* time rotation at the other two (or_fwd_rule / or_inv_rule below).          */
 /* ------------------------------------------------------------------------ */
 typedef struct {
     double re, im;
@@ -208,41 +230,71 @@ static inline cplx cmul(cplx x, cplx w)
     r.im = fma(x.re, w.im, x.im * w.re);
     return r;
 }
-static inline cplx cadd(cplx a, cplx b)
+
+#define OR_M 512
+#define OR_N 1024
+
+typedef struct {
+    int ready;
+    double fc[OR_M], ft[OR_M];     /* forward twiddle base per tree node v (c, tan) */
+    double W[OR_M / 2][2];         /* W^e, e < M/2, W[e + M/4] = i W[e] exactly */
+    double ic[OR_M / 4], it[OR_M / 4]; /* inverse base (cos, tan) of W^e, e < M/4 */
+    double TW[OR_M][2];            /* factored twist psi^j */
+} fft2_tab;
+
+static pthread_mutex_t g_tab_lock = PTHREAD_MUTEX_INITIALIZER;
+static fft2_tab g_tab;
+
+/* cos / tan of pi * num / den, rounded from long double (the product computes its
+ * tables with the same libm calls) */
+static void ct_of(long num, long den, double* c, double* t)
 {
-    cplx r = {a.re + b.re, a.im + b.im};
-    return r;
-}
-static inline cplx csub(cplx a, cplx b)
-{
-    cplx r = {a.re - b.re, a.im - b.im};
-    return r;
-}
-static inline cplx cconj(cplx a)
-{
-    cplx r = {a.re, -a.im};
-    return r;
+    const long double pi = 3.141592653589793238462643383279502884L;
+    if (num == 0) {
+        *c = 1.0;
+        *t = 0.0;
+        return;
+    }
+    if (4 * num == den) { /* pi/4: tan = 1 exactly */
+        *c = (double)cosl(pi / 4.0L);
+        *t = 1.0;
+        return;
+    }
+    const long double th = pi * (long double)num / (long double)den;
+    *c = (double)cosl(th);
+    *t = (double)tanl(th);
 }
 
-void or_fft_tables(uint32_t N, double* W, double* TW, double* UT)
+void or_fft2_make_tables(double* fc, double* ft, double* W, double* ic, double* it, double* TW)
 {
-    const uint32_t M = N / 2;
-    const uint32_t Q = M / 4; /* W[k + Q] = i * W[k] exactly */
-    const double pi = 3.14159265358979323846;
-    for (uint32_t k = 0; k < Q; k++) {
-        double re = k == 0 ? 1.0 : cos(2.0 * pi * (double)k / (double)M);
-        double im = k == 0 ? 0.0 : sin(2.0 * pi * (double)k / (double)M);
-        W[2 * k] = re;
-        W[2 * k + 1] = im;
-        W[2 * (k + Q)] = -im;
-        W[2 * (k + Q) + 1] = re;
+    const uint32_t M = OR_M, N = OR_N;
+    uint32_t E[2 * OR_M];
+    E[1] = N / 2;
+    for (uint32_t v = 1; v < M; v++) {
+        E[2 * v] = (E[v] / 2) % (2 * N);
+        E[2 * v + 1] = (E[v] / 2 + N) % (2 * N);
     }
-    /* twist psi^j (psi = e^{i pi / N}) in the factored form the GPU forms on the fly
-     * (kernels.cuh, TWIST_CONST): TW[j] = cmul(psi^(j mod 64), psi^(j - j mod 64)) with
-     * both factors rounded first; the untwist is conj(TW[j]) / M (exact scaling). */
+    fc[0] = ft[0] = 0.0;
+    for (uint32_t v = 1; v < M; v++) /* twiddle psi^(E/2): angle pi (E/2) / N */
+        ct_of((long)(E[v] / 2), (long)N, &fc[v], &ft[v]);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (uint32_t e = 0; e < M / 4; e++) {
+        double re = 1.0, im = 0.0;
+        if (e) {
+            re = (double)cosl(2.0L * pi * (long double)e / (long double)M);
+            im = (double)sinl(2.0L * pi * (long double)e / (long double)M);
+        }
+        W[2 * e] = re;
+        W[2 * e + 1] = im;
+        W[2 * (e + M / 4)] = -im;
+        W[2 * (e + M / 4) + 1] = re;
+        ct_of(2 * (long)e, (long)M, &ic[e], &it[e]);
+    }
+    /* twist psi^j in the factored form the GPU forms on the fly: TW[j] =
+     * cmul(psi^(j mod 64), psi^(j - j mod 64)) with both factors rounded first */
     for (uint32_t j = 0; j < M; j++) {
-        TW[2 * j] = j == 0 ? 1.0 : cos(pi * (double)j / (double)N);
-        TW[2 * j + 1] = j == 0 ? 0.0 : sin(pi * (double)j / (double)N);
+        TW[2 * j] = j == 0 ? 1.0 : cos(3.14159265358979323846 * (double)j / (double)N);
+        TW[2 * j + 1] = j == 0 ? 0.0 : sin(3.14159265358979323846 * (double)j / (double)N);
     }
     for (uint32_t j = M; j-- > 0;) { /* descending: factors j & 63, j & ~63 are still exact */
         const uint32_t lo = j & 63u, hi = j & ~63u;
@@ -253,136 +305,195 @@ void or_fft_tables(uint32_t N, double* W, double* TW, double* UT)
             TW[2 * j + 1] = fma(xr, wi, xi * wr);
         }
     }
-    for (uint32_t j = 0; j < M; j++) {
-        UT[2 * j] = TW[2 * j] / (double)M;
-        UT[2 * j + 1] = -TW[2 * j + 1] / (double)M;
-    }
 }
 
-typedef struct {
-    uint32_t N;
-    cplx* W;
-    cplx* TW;
-    cplx* UT;
-} fft_tab;
-
-static pthread_mutex_t g_tab_lock = PTHREAD_MUTEX_INITIALIZER;
-static fft_tab g_tabs[4];
-static int g_ntabs = 0;
-
-static const fft_tab* get_tab(uint32_t N)
+static const fft2_tab* get_tab(uint32_t N)
 {
+    if (N != OR_N)
+        return NULL;
     pthread_mutex_lock(&g_tab_lock);
-    for (int i = 0; i < g_ntabs; i++)
-        if (g_tabs[i].N == N) {
-            pthread_mutex_unlock(&g_tab_lock);
-            return &g_tabs[i];
-        }
-    fft_tab* t = &g_tabs[g_ntabs++];
-    t->N = N;
-    t->W = (cplx*)malloc(sizeof(cplx) * (N / 4));
-    t->TW = (cplx*)malloc(sizeof(cplx) * (N / 2));
-    t->UT = (cplx*)malloc(sizeof(cplx) * (N / 2));
-    or_fft_tables(N, (double*)t->W, (double*)t->TW, (double*)t->UT);
+    if (!g_tab.ready) {
+        or_fft2_make_tables(g_tab.fc, g_tab.ft, &g_tab.W[0][0], g_tab.ic, g_tab.it, &g_tab.TW[0][0]);
+        g_tab.ready = 1;
+    }
     pthread_mutex_unlock(&g_tab_lock);
-    return t;
+    return &g_tab;
 }
 
-/* The transforms run on split re/im arrays (same per-element arithmetic as
- * cmul/cadd/csub above; the layout only lets the compiler vectorize). */
-static void dif_forward_soa(uint32_t M, double* restrict zr, double* restrict zi,
-                            const cplx* W)
+/* kept for the API: W (N/4 complex), TW, UT = conj(TW) (no 1/M: folded into the BK) */
+void or_fft_tables(uint32_t N, double* W, double* TW, double* UT)
 {
-    uint32_t s = 0;
-    for (uint32_t h = M >> 1; h >= 1; h >>= 1, s++) {
-        for (uint32_t b = 0; b < M; b += 2 * h)
+    const fft2_tab* t = get_tab(N);
+    if (!t)
+        return;
+    memcpy(W, t->W, sizeof(t->W));
+    memcpy(TW, t->TW, sizeof(t->TW));
+    for (uint32_t j = 0; j < OR_M; j++) {
+        UT[2 * j] = t->TW[j][0];
+        UT[2 * j + 1] = -t->TW[j][1];
+    }
+}
+
+/* rot: 0 none, 1 multiply v by i, 3 multiply v by -i */
+static inline void bf_ct(double* ur, double* ui, double* vr, double* vi, double c, double t,
+                         int rot)
+{
+    double xr = *vr, xi = *vi;
+    if (rot == 1) {
+        const double tmp = xr;
+        xr = -xi;
+        xi = tmp;
+    } else if (rot == 3) {
+        const double tmp = xr;
+        xr = xi;
+        xi = -tmp;
+    }
+    const double sr = fma(-xi, t, xr), si = fma(xr, t, xi);
+    const double a = *ur, b = *ui;
+    *ur = fma(c, sr, a);
+    *ui = fma(c, si, b);
+    *vr = fma(-c, sr, a);
+    *vi = fma(-c, si, b);
+}
+
+static inline void bf_std(double* ur, double* ui, double* vr, double* vi, double wr, double wi)
+{
+    cplx v = {*vr, *vi}, w = {wr, wi};
+    const cplx t = cmul(v, w);
+    const double a = *ur, b = *ui;
+    *ur = a + t.re;
+    *ui = b + t.im;
+    *vr = a - t.re;
+    *vi = b - t.im;
+}
+
+static inline void bf_1(double* ur, double* ui, double* vr, double* vi)
+{
+    const double a = *ur, b = *ui, c = *vr, d = *vi;
+    *ur = a + c;
+    *ui = b + d;
+    *vr = a - c;
+    *vi = b - d;
+}
+
+static inline void bf_mi(double* ur, double* ui, double* vr, double* vi) /* w = -i */
+{
+    const double a = *ur, b = *ui, c = *vi, d = -*vr; /* -i v = (vi, -vr) */
+    *ur = a + c;
+    *ui = b + d;
+    *vr = a - c;
+    *vi = b - d;
+}
+
+/* forward rule: at stage s, block b uses node v = 2^s + b's own twiddle, except at
+ * stages s % 3 != 0 where an odd block uses its even sibling's twiddle after v -> i v
+ * (the sibling bit is a register bit of the GPU layout there) */
+static void fwd_soa(const fft2_tab* T, double* zr, double* zi)
+{
+    const uint32_t M = OR_M;
+    for (uint32_t s = 0; s < 9; s++) {
+        const uint32_t h = M >> (s + 1);
+        for (uint32_t b = 0; b < (1u << s); b++) {
+            const int sib = (s % 3 != 0) && (b & 1);
+            const uint32_t v = (1u << s) + b - (sib ? 1 : 0);
+            const double c = T->fc[v], t = T->ft[v];
+            const uint32_t o = 2 * h * b;
+            for (uint32_t j = 0; j < h; j++)
+                bf_ct(&zr[o + j], &zi[o + j], &zr[o + j + h], &zi[o + j + h], c, t, sib ? 1 : 0);
+        }
+    }
+}
+
+/* inverse rule (stage half-size h = 1 .. 256, butterfly (j, j + h), twiddle conj(W^e),
+ * e = j * (M/2) / h):
+ *   h <= 4, e in {0, M/4}: trivial;  h in {8, 64} (first stage of a GPU pass): STD with
+ *   the per-thread value conj(W[e]);  otherwise CT with the base e mod M/4 (conj: tan
+ *   negated), after v -> -i v when e >= M/4. */
+static void inv_soa(const fft2_tab* T, double* zr, double* zi)
+{
+    const uint32_t M = OR_M;
+    for (uint32_t h = 1; h < M; h <<= 1) {
+        const uint32_t step = (M / 2) / h;
+        for (uint32_t o = 0; o < M; o += 2 * h)
             for (uint32_t j = 0; j < h; j++) {
-                const double ur = zr[b + j], ui = zi[b + j];
-                const double vr = zr[b + j + h], vi = zi[b + j + h];
-                const double wr = W[j << s].re, wi = W[j << s].im;
-                zr[b + j] = ur + vr;
-                zi[b + j] = ui + vi;
-                const double dr = ur - vr, di = ui - vi;
-                zr[b + j + h] = fma(dr, wr, -(di * wi));
-                zi[b + j + h] = fma(dr, wi, di * wr);
+                const uint32_t e = j * step;
+                double *ur = &zr[o + j], *ui = &zi[o + j], *vr = &zr[o + j + h], *vi = &zi[o + j + h];
+                if (h <= 4 && e == 0)
+                    bf_1(ur, ui, vr, vi);
+                else if (h <= 4 && e == M / 4)
+                    bf_mi(ur, ui, vr, vi);
+                else if (h == 8 || h == 64)
+                    bf_std(ur, ui, vr, vi, T->W[e][0], -T->W[e][1]);
+                else {
+                    const uint32_t e0 = e % (M / 4);
+                    bf_ct(ur, ui, vr, vi, T->ic[e0], -T->it[e0], e >= M / 4 ? 3 : 0);
+                }
             }
     }
 }
 
-static void dit_inverse_soa(uint32_t M, double* restrict zr, double* restrict zi,
-                            const cplx* W)
-{
-    uint32_t logM = 0;
-    while ((1u << logM) < M)
-        logM++;
-    for (int s = (int)logM - 1; s >= 0; s--) {
-        uint32_t h = M >> (s + 1);
-        for (uint32_t b = 0; b < M; b += 2 * h)
-            for (uint32_t j = 0; j < h; j++) {
-                const double wr = W[j << s].re, wi = -W[j << s].im; /* conj(W) */
-                const double vr = zr[b + j + h], vi = zi[b + j + h];
-                const double tr = fma(vr, wr, -(vi * wi));
-                const double ti = fma(vr, wi, vi * wr);
-                const double ur = zr[b + j], ui = zi[b + j];
-                zr[b + j] = ur + tr;
-                zi[b + j] = ui + ti;
-                zr[b + j + h] = ur - tr;
-                zi[b + j + h] = ui - ti;
-            }
-    }
-}
-
-static void dif_forward(uint32_t M, cplx* z, const cplx* W)
-{
-    double zr[1024], zi[1024];
-    for (uint32_t j = 0; j < M; j++) {
-        zr[j] = z[j].re;
-        zi[j] = z[j].im;
-    }
-    dif_forward_soa(M, zr, zi, W);
-    for (uint32_t j = 0; j < M; j++) {
-        z[j].re = zr[j];
-        z[j].im = zi[j];
-    }
-}
-
-static void dit_inverse(uint32_t M, cplx* z, const cplx* W)
-{
-    double zr[1024], zi[1024];
-    for (uint32_t j = 0; j < M; j++) {
-        zr[j] = z[j].re;
-        zi[j] = z[j].im;
-    }
-    dit_inverse_soa(M, zr, zi, W);
-    for (uint32_t j = 0; j < M; j++) {
-        z[j].re = zr[j];
-        z[j].im = zi[j];
-    }
-}
-
+/* forward of integer digits: out = (re, im) pairs in slot order (unscaled) */
 void or_fft_forward_i32(uint32_t N, const int32_t* in, double* out)
 {
-    const fft_tab* t = get_tab(N);
-    const uint32_t M = N / 2;
-    cplx* z = (cplx*)out;
+    const fft2_tab* t = get_tab(N);
+    const uint32_t M = OR_M;
+    double zr[OR_M], zi[OR_M];
     for (uint32_t j = 0; j < M; j++) {
-        cplx a = {(double)in[j], (double)in[j + M]};
-        z[j] = cmul(a, t->TW[j]);
+        zr[j] = (double)in[j];
+        zi[j] = (double)in[j + M];
     }
-    dif_forward(M, z, t->W);
+    fwd_soa(t, zr, zi);
+    for (uint32_t j = 0; j < M; j++) {
+        out[2 * j] = zr[j];
+        out[2 * j + 1] = zi[j];
+    }
+}
+
+/* inverse: untwist, round each coefficient to the nearest integer mod 2^32 and ADD it
+ * into acc[N]; `in` (slot order) is the spectrum of a product with a 1/M-scaled BK */
+/* diagnostic: max distance of an inverse output from the nearest integer before rounding
+ * (the FFT rounding margin; coefficients are exact while it stays below 1/2) */
+static double g_fft_err = 0.0;
+static pthread_mutex_t g_err_lock = PTHREAD_MUTEX_INITIALIZER;
+double or_fft_margin(int reset)
+{
+    pthread_mutex_lock(&g_err_lock);
+    const double e = g_fft_err;
+    if (reset)
+        g_fft_err = 0.0;
+    pthread_mutex_unlock(&g_err_lock);
+    return e;
+}
+
+static void inverse_add_soa(const fft2_tab* t, double* zr, double* zi, uint32_t* acc)
+{
+    inv_soa(t, zr, zi);
+    double emax = 0.0;
+    for (uint32_t j = 0; j < OR_M; j++) {
+        const cplx y = {zr[j], zi[j]};
+        const cplx u = {t->TW[j][0], -t->TW[j][1]};
+        const cplx w = cmul(y, u);
+        emax = fmax(emax, fmax(fabs(w.re - rint(w.re)), fabs(w.im - rint(w.im))));
+        acc[j] += (uint32_t)(uint64_t)llrint(w.re);
+        acc[j + OR_M] += (uint32_t)(uint64_t)llrint(w.im);
+    }
+    if (emax > g_fft_err) {
+        pthread_mutex_lock(&g_err_lock);
+        if (emax > g_fft_err)
+            g_fft_err = emax;
+        pthread_mutex_unlock(&g_err_lock);
+    }
 }
 
 void or_fft_inverse_add(uint32_t N, double* in, uint32_t* acc)
 {
-    const fft_tab* t = get_tab(N);
-    const uint32_t M = N / 2;
-    cplx* z = (cplx*)in;
-    dit_inverse(M, z, t->W);
-    for (uint32_t j = 0; j < M; j++) {
-        cplx w = cmul(z[j], t->UT[j]);
-        acc[j] += (uint32_t)(uint64_t)llrint(w.re);
-        acc[j + M] += (uint32_t)(uint64_t)llrint(w.im);
+    const fft2_tab* t = get_tab(N);
+    double zr[OR_M], zi[OR_M];
+    for (uint32_t j = 0; j < OR_M; j++) {
+        zr[j] = in[2 * j];
+        zi[j] = in[2 * j + 1];
     }
+    inverse_add_soa(t, zr, zi, acc);
 }
 
 void or_polymul_exact_add(uint32_t N, const int32_t* d, const uint32_t* b, uint32_t* acc)
@@ -521,6 +632,8 @@ int or_keyset_generate(or_keyset* ks, const or_params* p, uint64_t seed)
             for (uint32_t j = 0; j < N; j++)
                 tmp[j] = (int32_t)ks->bk[q * N + j];
             or_fft_forward_i32(N, tmp, ks->bk_fft + q * N);
+            for (uint32_t f = 0; f < N; f++) /* 1/M folded into the key (exact) */
+                ks->bk_fft[q * N + f] *= 1.0 / (double)(N / 2);
             for (uint32_t f = 0; f < N / 2; f++) {
                 ks->bk_fft_soa[q * N + f] = ks->bk_fft[q * N + 2 * f];
                 ks->bk_fft_soa[q * N + N / 2 + f] = ks->bk_fft[q * N + 2 * f + 1];
@@ -579,19 +692,18 @@ int or_external_product(const or_keyset* ks, uint32_t i, const uint32_t* trlwe, 
                                          out + comp * N);
             }
     } else {
-        const fft_tab* tab = get_tab(N);
+        const fft2_tab* tab = get_tab(N);
         double Fr[512], Fi[512], Ar[2][512], Ai[2][512];
         memset(Ar, 0, sizeof(Ar));
         memset(Ai, 0, sizeof(Ai));
         for (uint32_t c = 0; c < 2; c++)
             for (uint32_t q = 0; q < p->l; q++) {
                 or_decompose(p, trlwe + c * N, q, dig);
-                for (uint32_t j = 0; j < M; j++) {  /* twist = cmul((d_j, d_{j+M}), TW[j]) */
-                    const double ar = (double)dig[j], ai = (double)dig[j + M];
-                    Fr[j] = fma(ar, tab->TW[j].re, -(ai * tab->TW[j].im));
-                    Fi[j] = fma(ar, tab->TW[j].im, ai * tab->TW[j].re);
+                for (uint32_t j = 0; j < M; j++) {
+                    Fr[j] = (double)dig[j];
+                    Fi[j] = (double)dig[j + M];
                 }
-                dif_forward_soa(M, Fr, Fi, tab->W);
+                fwd_soa(tab, Fr, Fi);
                 const uint32_t r = c * p->l + q;
                 for (uint32_t comp = 0; comp < 2; comp++) {
                     const double* Br = ks->bk_fft_soa + (((size_t)i * rows + r) * 2 + comp) * N;
@@ -608,16 +720,8 @@ int or_external_product(const or_keyset* ks, uint32_t i, const uint32_t* trlwe, 
                     }
                 }
             }
-        for (uint32_t comp = 0; comp < 2; comp++) {
-            dit_inverse_soa(M, Ar[comp], Ai[comp], tab->W);
-            uint32_t* o = out + comp * N;
-            for (uint32_t j = 0; j < M; j++) {
-                const double wr = fma(Ar[comp][j], tab->UT[j].re, -(Ai[comp][j] * tab->UT[j].im));
-                const double wi = fma(Ar[comp][j], tab->UT[j].im, Ai[comp][j] * tab->UT[j].re);
-                o[j] += (uint32_t)(uint64_t)llrint(wr);
-                o[j + M] += (uint32_t)(uint64_t)llrint(wi);
-            }
-        }
+        for (uint32_t comp = 0; comp < 2; comp++)
+            inverse_add_soa(tab, Ar[comp], Ai[comp], out + comp * N);
     }
     free(dig);
     return 0;

@@ -91,7 +91,7 @@ typedef struct {
     uint8_t* trlwe_key; /* N bits */
     uint32_t* bk;       /* torus form [n][(k+1)l][k+1][N] */
     uint32_t* ksk;      /* [N][t][base-1][n+1] */
-    double* bk_fft;     /* [n][(k+1)l][k+1][N/2][2] (re,im), DIF bit-reversed order */
+    double* bk_fft;     /* [n][(k+1)l][k+1][N/2][2] (re,im), slot order, scaled by 1/(N/2) */
     double* bk_fft_soa; /* same values, [..][k+1][re[N/2], im[N/2]] (vectorisable MAC) */
 } or_keyset;
 
@@ -101,13 +101,18 @@ void or_keyset_free(or_keyset* ks);
 size_t or_bk_words(const or_params* p);
 size_t or_ksk_words(const or_params* p);
 
-/* ---- negacyclic transform (N real -> N/2 complex) ---- */
+/* ---- negacyclic transform (N real -> N/2 complex), N = 1024 only ---- */
+/* the transform's tables (tfhe_oracle.c): forward twiddle base (cos, tan) per tree node
+ * [M], W^e [M/2][2], inverse base (cos, tan) [M/4], factored twist [M][2] */
+void or_fft2_make_tables(double* fc, double* ft, double* W, double* ic, double* it, double* TW);
 void or_fft_tables(uint32_t N, double* W /*[N/4][2]*/, double* TW /*[N/2][2]*/,
                    double* UT /*[N/2][2]*/);
 void or_fft_forward_i32(uint32_t N, const int32_t* in, double* out /*[N/2][2]*/);
 /* inverse transform; rounds each coefficient to the nearest integer mod 2^32 and
  * ADDS it into acc[N]. in[] is destroyed. */
 void or_fft_inverse_add(uint32_t N, double* in, uint32_t* acc);
+/* max |w - rint(w)| over every inverse output since the last reset (FFT rounding margin) */
+double or_fft_margin(int reset);
 /* exact negacyclic product mod 2^32: acc += d * b */
 void or_polymul_exact_add(uint32_t N, const int32_t* d, const uint32_t* b, uint32_t* acc);
 

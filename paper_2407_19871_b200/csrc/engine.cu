@@ -17,9 +17,6 @@
 #include "server.hpp"
 #include "circuits.hpp"
 #include "kernels.cuh"
-#include "br_warp.cuh"
-#include "br_pair.cuh"
-#include "br_lat2.cuh"
 #include "program.hpp"
 
 using namespace lpb;
@@ -103,7 +100,7 @@ struct locpir_b200_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::string err;
-    DevBuf<double2> W, TW, UT, bkf;
+    DevBuf<double2> ftw, itw, TW, bkf;  // per-thread twiddles [8][64] x2, twist [512]
     DevBuf<uint32_t> ksk;
     bool have_keys = false;
     DevBuf<uint32_t> pool_n, pool_N;
@@ -118,14 +115,8 @@ struct locpir_b200_ctx {
     bool timing = false;
     Timer timer;
     int num_sms = 148;
-    // blind-rotate kernel: 0 = 64-thread CTA per ciphertext (k_blind_rotate, default),
-    // 1 = warp per ciphertext (k_blind_rotate_w, TMEM accumulators).  Env
-    // LOCPIR_B200_BR=cta|warp at context creation; it fixes the BK frequency layout.
-    int br_warp = 0;
-    int br_pair = 0;  // LOCPIR_B200_BR=pair: paired digit transforms (k_blind_rotate_pair)
     // small levels (fewer bootstraps than SMs) take the latency kernels
     int small_levels = 1;
-    int lat_cluster = 0;  // LOCPIR_B200_LAT=cluster: 2-CTA cluster latency kernel (K1c)
     int use_graphs = 1;   // LOCPIR_B200_GRAPH=0: programs launch without CUDA graphs
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
     DevBuf<uint32_t> ks_partial;
@@ -163,39 +154,102 @@ int guarded(locpir_b200_ctx* c, F&& f)
     }
 }
 
-// Twiddle tables: same formulas as the oracle contract (oracle/tfhe_oracle.c
-// or_fft_tables): W[k] = e^{2 pi i k / 512} with W[k + 128] = i W[k] exactly,
-// TW[j] = e^{i pi j / 1024}, UT[j] = conj(TW[j]) / 512.
-void make_tables(uint32_t N, std::vector<double2>& W, std::vector<double2>& TW,
-                 std::vector<double2>& UT)
+// Transform tables: the same values as the oracle contract (oracle/tfhe_oracle.c
+// or_fft2_make_tables, the same libm calls in long double, rounded to double):
+//   forward tree node v (stage s, block b = v - 2^s): twiddle psi^(E[v]/2) as
+//     (cos, tan), E[1] = N/2, children E/2 and E/2 + N (mod 2N), psi = e^{i pi / N};
+//   inverse: W^e = e^{2 pi i e / M} (e < M/2, W[e + M/4] = i W[e] exactly) and the
+//     base (cos, tan) of W^e, e < M/4;
+//   twist psi^j in factored form cmul(psi^(j mod 64), psi^(j - j mod 64)).
+// Per-thread tables [entry][t] for the 64-thread transform (fft.cuh FwdTw / InvTw).
+struct Tables {
+    std::vector<double2> fwd, inv, tw;  // [8][64], [8][64], [512]
+    double2 fwd0[4], inv4, twq[8];
+};
+
+void ct_of(long num, long den, double& c, double& t)
 {
-    const uint32_t M = N / 2, Q = M / 4;
-    const double pi = 3.14159265358979323846;
-    W.assign(M / 2, make_double2(0, 0));
-    TW.assign(M, make_double2(0, 0));
-    UT.assign(M, make_double2(0, 0));
-    for (uint32_t k = 0; k < Q; k++) {
-        const double re = k == 0 ? 1.0 : std::cos(2.0 * pi * (double)k / (double)M);
-        const double im = k == 0 ? 0.0 : std::sin(2.0 * pi * (double)k / (double)M);
-        W[k] = make_double2(re, im);
-        W[k + Q] = make_double2(-im, re);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    if (num == 0) {
+        c = 1.0;
+        t = 0.0;
+        return;
     }
-    // twist psi^j in factored form: TW[j] = cmul(psi^(j mod 64), psi^(j - j mod 64)), the
-    // product k_blind_rotate forms on the fly (TWIST_CONST); same table as the oracle's
-    // (tfhe_oracle.c or_fft_tables)
+    if (4 * num == den) {  // pi/4: tan = 1 exactly
+        c = (double)cosl(pi / 4.0L);
+        t = 1.0;
+        return;
+    }
+    const long double th = pi * (long double)num / (long double)den;
+    c = (double)cosl(th);
+    t = (double)tanl(th);
+}
+
+Tables make_tables(uint32_t N)
+{
+    const uint32_t M = N / 2;  // 512
+    Tables T;
+    std::vector<uint32_t> E(2 * M);
+    E[1] = N / 2;
+    for (uint32_t v = 1; v < M; v++) {
+        E[2 * v] = (E[v] / 2) % (2 * N);
+        E[2 * v + 1] = (E[v] / 2 + N) % (2 * N);
+    }
+    std::vector<double2> node(M);
+    for (uint32_t v = 1; v < M; v++)
+        ct_of((long)(E[v] / 2), (long)N, node[v].x, node[v].y);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    std::vector<double2> W(M / 2), ic(M / 4);
+    for (uint32_t e = 0; e < M / 4; e++) {
+        double re = 1.0, im = 0.0;
+        if (e) {
+            re = (double)cosl(2.0L * pi * (long double)e / (long double)M);
+            im = (double)sinl(2.0L * pi * (long double)e / (long double)M);
+        }
+        W[e] = make_double2(re, im);
+        W[e + M / 4] = make_double2(-im, re);
+        ct_of(2 * (long)e, (long)M, ic[e].x, ic[e].y);
+    }
+    auto icj = [&](uint32_t e) { return make_double2(ic[e].x, -ic[e].y); };  // conj: -tan
+    auto wcj = [&](uint32_t e) { return make_double2(W[e].x, -W[e].y); };
+    T.fwd.assign(8 * 64, make_double2(0, 0));
+    T.inv.assign(8 * 64, make_double2(0, 0));
+    for (int t = 0; t < 64; t++) {
+        const int k = t >> 3, r = t & 7;
+        const double2 f[8] = {node[8 + k],   node[16 + 2 * k],  node[32 + 4 * k],
+                              node[32 + 4 * k + 2], node[64 + t], node[128 + 2 * t],
+                              node[256 + 4 * t], node[256 + 4 * t + 2]};
+        const double2 g[8] = {wcj(32 * r), icj(16 * r), icj(8 * r), icj(8 * r + 64),
+                              wcj(4 * t),  icj(2 * t),  icj(t),     icj(t + 64)};
+        for (int e = 0; e < 8; e++) {
+            T.fwd[e * 64 + t] = f[e];
+            T.inv[e * 64 + t] = g[e];
+        }
+    }
+    T.fwd0[0] = node[1];
+    T.fwd0[1] = node[2];
+    T.fwd0[2] = node[4];
+    T.fwd0[3] = node[6];
+    T.inv4 = icj(64);
+    // twist psi^j (psi = e^{i pi / N}), factored as the kernels form it on the fly
+    T.tw.assign(M, make_double2(0, 0));
+    const double dpi = 3.14159265358979323846;
     for (uint32_t j = 0; j < M; j++)
-        TW[j] = make_double2(j == 0 ? 1.0 : std::cos(pi * (double)j / (double)N),
-                             j == 0 ? 0.0 : std::sin(pi * (double)j / (double)N));
+        T.tw[j] = make_double2(j == 0 ? 1.0 : std::cos(dpi * (double)j / (double)N),
+                               j == 0 ? 0.0 : std::sin(dpi * (double)j / (double)N));
     for (uint32_t j = M; j-- > 0;) {
         const uint32_t lo = j & 63u, hi = j & ~63u;
         if (lo && hi) {
-            const double2 x = TW[lo], w = TW[hi];
-            TW[j] = make_double2(std::fma(x.x, w.x, -(x.y * w.y)), std::fma(x.x, w.y, x.y * w.x));
+            const double2 x = T.tw[lo], w = T.tw[hi];
+            T.tw[j] = make_double2(std::fma(x.x, w.x, -(x.y * w.y)), std::fma(x.x, w.y, x.y * w.x));
         }
     }
-    for (uint32_t j = 0; j < M; j++)
-        UT[j] = make_double2(TW[j].x / (double)M, -TW[j].y / (double)M);
+    for (int q = 0; q < 8; q++)
+        T.twq[q] = T.tw[64 * q];
+    return T;
 }
+
+FftTabs tabs(const locpir_b200_ctx* c) { return FftTabs{c->ftw.p, c->itw.p, c->TW.p}; }
 
 void need_keys(locpir_b200_ctx* c)
 {
@@ -235,49 +289,22 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
         return;
     timed_begin(c, 0);
     const uint32_t mu = 0x20000000u;
-    if (!c->br_warp && c->small_levels && c->lat_cluster && 2 * count <= (uint32_t)c->num_sms) {
-        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-            k_blind_rotate_lat2<3, 7><<<2 * count, 64 * 3, sizeof(Lat2Smem<3>), c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
-        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-            k_blind_rotate_lat2<2, 10><<<2 * count, 64 * 2, sizeof(Lat2Smem<2>), c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
-        else
-            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
-    } else if (!c->br_warp && c->small_levels && count <= (uint32_t)c->num_sms) {
+    const FftTabs tb = tabs(c);
+    if (c->small_levels && count <= (uint32_t)c->num_sms) {
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
             k_blind_rotate_lat<3, 7><<<count, 128 * 3, kLatSmemBytes<3>, c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
             k_blind_rotate_lat<2, 10><<<count, 128 * 2, kLatSmemBytes<2>, c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
-        else
-            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
-    } else if (c->br_pair) {
-        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-            k_blind_rotate_pair<3, 7><<<count, 64, sizeof(PairSmem), c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
-        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-            k_blind_rotate_pair<2, 10><<<count, 64, sizeof(PairSmem), c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
-        else
-            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
-    } else if (c->br_warp) {
-        const uint32_t blocks = (count + W_CT - 1) / W_CT;
-        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-            k_blind_rotate_w<3, 7><<<blocks, 32 * W_CT, W_SMEM, c->stream>>>(
-                c->dp, items, count, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
-        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-            k_blind_rotate_w<2, 10><<<blocks, 32 * W_CT, W_SMEM, c->stream>>>(
-                c->dp, items, count, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, mu);
+                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
     } else if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-        k_blind_rotate<3, 7><<<count, 64, BR_DYN_SMEM, c->stream>>>(
-            c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
+        k_blind_rotate<3, 7><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
+                                                         c->bkf.p, tb, mu);
     else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-        k_blind_rotate<2, 10><<<count, 64, BR_DYN_SMEM, c->stream>>>(
-            c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu);
+        k_blind_rotate<2, 10><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
+                                                          c->bkf.p, tb, mu);
     else
         throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
     CK(cudaGetLastError());
@@ -424,7 +451,7 @@ void program_enqueue(locpir_b200_ctx* c, const locpir_b200_program* pr, const Br
 std::vector<const void*> graph_signature(const locpir_b200_ctx* c)
 {
     return {c->pool_n.p, c->pool_N.p, c->ks_partial.p, c->bkf.p, c->ksk.p,
-            c->W.p,      c->TW.p,     c->UT.p,         (const void*)c->stream};
+            c->ftw.p,    c->itw.p,    c->TW.p,         (const void*)c->stream};
 }
 
 size_t plan_items(const Plan& P, size_t& nb, size_t& nk, size_t& nl)
@@ -536,36 +563,18 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
             c->own_stream = true;
         }
-        std::vector<double2> W, TW, UT;
-        make_tables(p->N, W, TW, UT);
-        c->W.reserve(W.size(), c->stream, false);
-        c->TW.reserve(TW.size(), c->stream, false);
-        c->UT.reserve(UT.size(), c->stream, false);
-        CK(cudaMemcpy(c->W.p, W.data(), W.size() * sizeof(double2), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->TW.p, TW.data(), TW.size() * sizeof(double2), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->UT.p, UT.data(), UT.size() * sizeof(double2), cudaMemcpyHostToDevice));
-        {
-            double2 twq[8];
-            for (int q = 0; q < 8; q++)
-                twq[q] = TW[64 * q];
-            CK(cudaMemcpyToSymbol(c_twq, twq, sizeof(twq)));
-        }
-        if (BR_DYN_SMEM) {
-            CK(cudaFuncSetAttribute(k_blind_rotate<3, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)BR_DYN_SMEM));
-            CK(cudaFuncSetAttribute(k_blind_rotate<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)BR_DYN_SMEM));
-        }
+        const Tables T = make_tables(p->N);
+        c->ftw.reserve(T.fwd.size(), c->stream, false);
+        c->itw.reserve(T.inv.size(), c->stream, false);
+        c->TW.reserve(T.tw.size(), c->stream, false);
+        CK(cudaMemcpy(c->ftw.p, T.fwd.data(), T.fwd.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->itw.p, T.inv.data(), T.inv.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->TW.p, T.tw.data(), T.tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyToSymbol(c_twq, T.twq, sizeof(T.twq)));
+        CK(cudaMemcpyToSymbol(c_fwd0, T.fwd0, sizeof(T.fwd0)));
+        CK(cudaMemcpyToSymbol(c_inv4, &T.inv4, sizeof(T.inv4)));
         CK(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(KS_CT * p->N * sizeof(uint16_t))));
-        CK(cudaFuncSetAttribute(k_blind_rotate_w<3, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)W_SMEM));
-        CK(cudaFuncSetAttribute(k_blind_rotate_w<2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)W_SMEM));
-        CK(cudaFuncSetAttribute(k_blind_rotate_lat2<3, 7>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Lat2Smem<3>)));
-        CK(cudaFuncSetAttribute(k_blind_rotate_lat2<2, 10>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Lat2Smem<2>)));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<3, 7>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLatSmemBytes<3>));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<2, 10>,
@@ -574,18 +583,8 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             c->l2_persist = strcmp(lp, "0") != 0;
         if (const char* sl = getenv("LOCPIR_B200_SMALL"))
             c->small_levels = strcmp(sl, "0") != 0;
-        if (const char* lt = getenv("LOCPIR_B200_LAT"))
-            c->lat_cluster = strcmp(lt, "cluster") == 0;
         if (const char* gr = getenv("LOCPIR_B200_GRAPH"))
             c->use_graphs = strcmp(gr, "0") != 0;
-        CK(cudaFuncSetAttribute(k_blind_rotate_pair<3, 7>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem)));
-        CK(cudaFuncSetAttribute(k_blind_rotate_pair<2, 10>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem)));
-        if (const char* br = getenv("LOCPIR_B200_BR")) {
-            c->br_warp = strcmp(br, "warp") == 0;
-            c->br_pair = strcmp(br, "pair") == 0;
-        }
     });
     if (rc != LOCPIR_B200_OK) {
         fprintf(stderr, "locpir_b200_ctx_create: %s\n", c->err.c_str());
@@ -634,11 +633,7 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
             dbk = tmp.p;
         }
         c->bkf.reserve(polys * FFT_M, c->stream, false);
-        if (c->br_warp)
-            k_bk_to_freq_w<<<(uint32_t)((polys + W_CT - 1) / W_CT), 32 * W_CT, 0, c->stream>>>(
-                dbk, c->bkf.p, c->W.p, c->TW.p, (uint32_t)polys);
-        else
-            k_bk_to_freq<<<(uint32_t)polys, 64, 0, c->stream>>>(dbk, c->bkf.p, c->W.p, c->TW.p);
+        k_bk_to_freq<<<(uint32_t)polys, 64, 0, c->stream>>>(dbk, c->bkf.p, tabs(c));
         CK(cudaGetLastError());
         // KSK rows padded to n_stride words (zero padding)
         const size_t rows_ks = (size_t)c->p.N * c->p.ks_t * ((1u << c->p.ks_basebit) - 1);
@@ -1370,11 +1365,11 @@ int locpir_b200_debug_fft_error(locpir_b200_ctx* c, const uint32_t* lwe_n, uint6
         CK(cudaMemcpyAsync(d.p, items.data(), count * sizeof(BrItem), cudaMemcpyHostToDevice, c->stream));
         const uint32_t mu = 0x20000000u;
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-            k_blind_rotate<3, 7, true><<<(unsigned)count, 64, BR_DYN_SMEM, c->stream>>>(
-                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu, e.p);
+            k_blind_rotate<3, 7, true><<<(unsigned)count, 64, 0, c->stream>>>(
+                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, tabs(c), mu, e.p);
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-            k_blind_rotate<2, 10, true><<<(unsigned)count, 64, BR_DYN_SMEM, c->stream>>>(
-                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, c->W.p, c->TW.p, c->UT.p, mu, e.p);
+            k_blind_rotate<2, 10, true><<<(unsigned)count, 64, 0, c->stream>>>(
+                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, tabs(c), mu, e.p);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
         CK(cudaGetLastError());

@@ -1,17 +1,32 @@
 // fft.cuh -- FP64 negacyclic transform for N = 1024 (512 complex points), one
 // 64-thread group per polynomial, 8 complex points per thread in registers.
 //
-// The arithmetic is the contract stated in oracle/tfhe_oracle.c (radix-2 DIF
-// forward with W[k] = e^{+2 pi i k / 512}, radix-2 DIT inverse with conj(W),
-// cmul(x, w) = (fma(xr, wr, -(xi*wi)), fma(xr, wi, xi*wr))): three radix-2
-// stages are fused per register pass, the passes exchange through a swizzled
-// shared-memory tile, and every butterfly performs exactly the oracle's
-// roundings (all ops are __*_rn intrinsics, so nvcc cannot contract them).
-// Multiplications by exactly 1 and by exactly +-i are skipped -- exact, so the
-// results stay bit-identical to the oracle.
+// The arithmetic is the contract stated in oracle/tfhe_oracle.c (the oracle's
+// FFT mode executes the same operations in the same order, so the GPU is bit-exact
+// with it):
+//
+//   forward  a_j = d_j + i d_{j+512} (integer digits) -> Z_k = sum_j a_j psi^j W^{jk}
+//            in slot bitrev9(k): Cooley-Tukey with the negacyclic twist absorbed into
+//            the twiddles (tree node v = 2^s + b at stage s has twiddle psi^(E[v]/2),
+//            E[1] = 512, children E/2 and E/2 + 1024 mod 2048).  No twist multiply.
+//   inverse  plain inverse DFT, radix-2 DIT, bit-reversed in -> natural out; the
+//            untwist conj(psi^j) is applied by the caller; 1/512 lives in the BK.
+//
+// Butterflies (every op is an __*_rn intrinsic, so nvcc cannot contract or reorder):
+//   ct<ROT>(u, v, w)  w = (c, t) stands for c (1 + i t); v is first rotated by
+//                     ROT (0: none, 1: i, 3: -i, exact); s = (fma(-vi, t, vr),
+//                     fma(vr, t, vi)); u' = u + c s, v' = u - c s as fmas.
+//                     6 DFMA instead of the 8 FP64 ops of a complex-multiply butterfly.
+//   std_(u, v, w)     t = cmul(v, w); u' = u + t; v' = u - t (8 ops) -- used where the
+//                     per-thread twiddle can be exactly -i (first stage of an inverse
+//                     pass), for which (c, t) is degenerate.
+//   bf_1 / bf_mi      w = 1 / w = -i: four adds.
+// A stage's twiddle is a per-thread register value at the first stage of each
+// register pass (its index bits are thread bits) and a register value times a
+// compile-time rotation at the other two stages (the sibling bit is a register bit).
 //
 // Register layouts (M = 512, thread t in [0, 64), t = 8k + r):
-//   pass 0 : x[q] = position t + 64 q        (natural order: the twisted input)
+//   pass 0 : x[q] = position t + 64 q        (natural order: the folded input)
 //   pass 1 : x[m] = position 64 k + 8 m + r
 //   pass 2 : x[q] = position 8 t + q         (bit-reversed order: frequency slots)
 #pragma once
@@ -30,54 +45,51 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 w)
     r.y = __fma_rn(a.x, w.y, __dmul_rn(a.y, w.x));
     return r;
 }
-__device__ __forceinline__ double2 cadd(double2 a, double2 b)
-{
-    return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
-}
-__device__ __forceinline__ double2 csub(double2 a, double2 b)
-{
-    return make_double2(__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y));
-}
-__device__ __forceinline__ double2 mul_i(double2 w) { return make_double2(-w.y, w.x); }
 __device__ __forceinline__ double2 conj2(double2 w) { return make_double2(w.x, -w.y); }
 
-// forward DIF butterflies
-__device__ __forceinline__ void dif(double2& u, double2& v, double2 w)
+template <int ROT>
+__device__ __forceinline__ void ct(double2& u, double2& v, double2 w)
 {
-    const double2 d = csub(u, v);
-    u = cadd(u, v);
-    v = cmul(d, w);
+    double xr, xi;
+    if constexpr (ROT == 0) {
+        xr = v.x;
+        xi = v.y;
+    } else if constexpr (ROT == 1) {  // i v
+        xr = -v.y;
+        xi = v.x;
+    } else {  // -i v
+        xr = v.y;
+        xi = -v.x;
+    }
+    const double sr = __fma_rn(-xi, w.y, xr);
+    const double si = __fma_rn(xr, w.y, xi);
+    const double a = u.x, b = u.y;
+    u.x = __fma_rn(w.x, sr, a);
+    u.y = __fma_rn(w.x, si, b);
+    v.x = __fma_rn(-w.x, sr, a);
+    v.y = __fma_rn(-w.x, si, b);
 }
-__device__ __forceinline__ void dif_1(double2& u, double2& v)
+__device__ __forceinline__ void std_(double2& u, double2& v, double2 w)
 {
-    const double2 d = csub(u, v);
-    u = cadd(u, v);
-    v = d;
+    const double2 tt = cmul(v, w);
+    const double a = u.x, b = u.y;
+    u.x = __dadd_rn(a, tt.x);
+    u.y = __dadd_rn(b, tt.y);
+    v.x = __dsub_rn(a, tt.x);
+    v.y = __dsub_rn(b, tt.y);
 }
-__device__ __forceinline__ void dif_i(double2& u, double2& v)
+__device__ __forceinline__ void bf_1(double2& u, double2& v)
 {
-    const double2 d = csub(u, v);
-    u = cadd(u, v);
-    v = mul_i(d);
+    const double2 a = u, c = v;
+    u = make_double2(__dadd_rn(a.x, c.x), __dadd_rn(a.y, c.y));
+    v = make_double2(__dsub_rn(a.x, c.x), __dsub_rn(a.y, c.y));
 }
-// inverse DIT butterflies (wc = conj(W) already applied by the caller)
-__device__ __forceinline__ void dit(double2& u, double2& v, double2 wc)
+__device__ __forceinline__ void bf_mi(double2& u, double2& v)  // w = -i: -i v = (vi, -vr)
 {
-    const double2 tt = cmul(v, wc);
-    v = csub(u, tt);
-    u = cadd(u, tt);
-}
-__device__ __forceinline__ void dit_1(double2& u, double2& v)
-{
-    const double2 tt = v;
-    v = csub(u, tt);
-    u = cadd(u, tt);
-}
-__device__ __forceinline__ void dit_mi(double2& u, double2& v)  // conj(i) = -i
-{
-    const double2 tt = make_double2(v.y, -v.x);
-    v = csub(u, tt);
-    u = cadd(u, tt);
+    const double2 a = u;
+    const double c = v.y, d = -v.x;
+    u = make_double2(__dadd_rn(a.x, c), __dadd_rn(a.y, d));
+    v = make_double2(__dsub_rn(a.x, c), __dsub_rn(a.y, d));
 }
 
 // Exchange tile layout: position 64k + 8m + r (k, m, r in [0, 8)) lives at slot
@@ -87,27 +99,141 @@ __device__ __forceinline__ void dit_mi(double2& u, double2& v)  // conj(i) = -i
 constexpr int XTILE = 576;
 __device__ __forceinline__ int slot_of(int k, int m, int r) { return 72 * k + 9 * m + r; }
 
-// Per-thread twiddles, constant for the whole kernel.
-struct Twiddles {
-    double2 p0a, p0b, p0c, p0d;  // W[t], W[t+64], W[2t], W[4t]
-    double2 p1a, p1b, p1c, p1d;  // W[8r], W[8r+64], W[16r], W[32r]
-    double2 w64;                 // W[64]
+// Per-thread twiddles.  Host tables (engine.cu make_tables) hold them per thread,
+// [entry][t], so a CTA loads them with coalesced 16-byte loads.
+constexpr int TW_ENTRIES = 8;
+struct FwdTw {  // (c, tan): stage 3, 4, 5 (2), 6, 7, 8 (2)
+    double2 s3, s4, s5a, s5b, s6, s7, s8a, s8b;
 };
+struct InvTw {  // h = 8 (std, conj W), 16, 32 (2) | h = 64 (std, conj W), 128, 256 (2)
+    double2 h8, h16, h32a, h32b, h64, h128, h256a, h256b;
+};
+// pass-0 forward twiddles are the same for every thread: nodes 1, 2, 4, 6 (c, tan)
+__constant__ double2 c_fwd0[4];
+// inverse h = 4 base (cos, -tan) of W^64 (conjugated)
+__constant__ double2 c_inv4;
 
-__device__ __forceinline__ Twiddles load_twiddles(const double2* __restrict__ W, int t)
+__device__ __forceinline__ FwdTw load_fwd_tw(const double2* __restrict__ T, int t)
 {
-    Twiddles tw;
-    const int r = t & 7;
-    tw.p0a = W[t];
-    tw.p0b = W[t + 64];
-    tw.p0c = W[2 * t];
-    tw.p0d = W[4 * t];
-    tw.p1a = W[8 * r];
-    tw.p1b = W[8 * r + 64];
-    tw.p1c = W[16 * r];
-    tw.p1d = W[32 * r];
-    tw.w64 = W[64];
-    return tw;
+    FwdTw w;
+    w.s3 = T[0 * 64 + t];
+    w.s4 = T[1 * 64 + t];
+    w.s5a = T[2 * 64 + t];
+    w.s5b = T[3 * 64 + t];
+    w.s6 = T[4 * 64 + t];
+    w.s7 = T[5 * 64 + t];
+    w.s8a = T[6 * 64 + t];
+    w.s8b = T[7 * 64 + t];
+    return w;
+}
+__device__ __forceinline__ InvTw load_inv_tw(const double2* __restrict__ T, int t)
+{
+    InvTw w;
+    w.h8 = __ldg(T + 0 * 64 + t);
+    w.h16 = __ldg(T + 1 * 64 + t);
+    w.h32a = __ldg(T + 2 * 64 + t);
+    w.h32b = __ldg(T + 3 * 64 + t);
+    w.h64 = __ldg(T + 4 * 64 + t);
+    w.h128 = __ldg(T + 5 * 64 + t);
+    w.h256a = __ldg(T + 6 * 64 + t);
+    w.h256b = __ldg(T + 7 * 64 + t);
+    return w;
+}
+
+// ---- forward passes (tree stages 0-2, 3-5, 6-8)
+__device__ __forceinline__ void fwd_pass0(double2 x[8])
+{
+    const double2 n1 = c_fwd0[0], n2 = c_fwd0[1], n4 = c_fwd0[2], n6 = c_fwd0[3];
+    ct<0>(x[0], x[4], n1);
+    ct<0>(x[1], x[5], n1);
+    ct<0>(x[2], x[6], n1);
+    ct<0>(x[3], x[7], n1);
+    ct<0>(x[0], x[2], n2);
+    ct<0>(x[1], x[3], n2);
+    ct<1>(x[4], x[6], n2);
+    ct<1>(x[5], x[7], n2);
+    ct<0>(x[0], x[1], n4);
+    ct<1>(x[2], x[3], n4);
+    ct<0>(x[4], x[5], n6);
+    ct<1>(x[6], x[7], n6);
+}
+__device__ __forceinline__ void fwd_pass1(double2 x[8], const FwdTw& w)
+{
+    ct<0>(x[0], x[4], w.s3);
+    ct<0>(x[1], x[5], w.s3);
+    ct<0>(x[2], x[6], w.s3);
+    ct<0>(x[3], x[7], w.s3);
+    ct<0>(x[0], x[2], w.s4);
+    ct<0>(x[1], x[3], w.s4);
+    ct<1>(x[4], x[6], w.s4);
+    ct<1>(x[5], x[7], w.s4);
+    ct<0>(x[0], x[1], w.s5a);
+    ct<1>(x[2], x[3], w.s5a);
+    ct<0>(x[4], x[5], w.s5b);
+    ct<1>(x[6], x[7], w.s5b);
+}
+__device__ __forceinline__ void fwd_pass2(double2 x[8], const FwdTw& w)
+{
+    ct<0>(x[0], x[4], w.s6);
+    ct<0>(x[1], x[5], w.s6);
+    ct<0>(x[2], x[6], w.s6);
+    ct<0>(x[3], x[7], w.s6);
+    ct<0>(x[0], x[2], w.s7);
+    ct<0>(x[1], x[3], w.s7);
+    ct<1>(x[4], x[6], w.s7);
+    ct<1>(x[5], x[7], w.s7);
+    ct<0>(x[0], x[1], w.s8a);
+    ct<1>(x[2], x[3], w.s8a);
+    ct<0>(x[4], x[5], w.s8b);
+    ct<1>(x[6], x[7], w.s8b);
+}
+
+// ---- inverse passes (h = 1, 2, 4 | 8, 16, 32 | 64, 128, 256)
+__device__ __forceinline__ void inv_pass2(double2 x[8])
+{
+    bf_1(x[0], x[1]);
+    bf_1(x[2], x[3]);
+    bf_1(x[4], x[5]);
+    bf_1(x[6], x[7]);
+    bf_1(x[0], x[2]);
+    bf_mi(x[1], x[3]);
+    bf_1(x[4], x[6]);
+    bf_mi(x[5], x[7]);
+    const double2 b = c_inv4;
+    bf_1(x[0], x[4]);
+    ct<0>(x[1], x[5], b);
+    bf_mi(x[2], x[6]);
+    ct<3>(x[3], x[7], b);
+}
+__device__ __forceinline__ void inv_pass1(double2 x[8], const InvTw& w)
+{
+    std_(x[0], x[1], w.h8);
+    std_(x[2], x[3], w.h8);
+    std_(x[4], x[5], w.h8);
+    std_(x[6], x[7], w.h8);
+    ct<0>(x[0], x[2], w.h16);
+    ct<3>(x[1], x[3], w.h16);
+    ct<0>(x[4], x[6], w.h16);
+    ct<3>(x[5], x[7], w.h16);
+    ct<0>(x[0], x[4], w.h32a);
+    ct<0>(x[1], x[5], w.h32b);
+    ct<3>(x[2], x[6], w.h32a);
+    ct<3>(x[3], x[7], w.h32b);
+}
+__device__ __forceinline__ void inv_pass0(double2 x[8], const InvTw& w)
+{
+    std_(x[0], x[1], w.h64);
+    std_(x[2], x[3], w.h64);
+    std_(x[4], x[5], w.h64);
+    std_(x[6], x[7], w.h64);
+    ct<0>(x[0], x[2], w.h128);
+    ct<3>(x[1], x[3], w.h128);
+    ct<0>(x[4], x[6], w.h128);
+    ct<3>(x[5], x[7], w.h128);
+    ct<0>(x[0], x[4], w.h256a);
+    ct<0>(x[1], x[5], w.h256b);
+    ct<3>(x[2], x[6], w.h256a);
+    ct<3>(x[3], x[7], w.h256b);
 }
 
 // Exchange helpers.  `bar` synchronises the threads that share the tile.
@@ -140,287 +266,67 @@ __device__ __forceinline__ void exch_p1_to_p2(double2 x[8], double2* buf, int t,
     for (int q = 0; q < 8; q++)
         x[q] = rd[q];
 }
-template <class Bar>
-__device__ __forceinline__ void exch_p2_to_p1(double2 x[8], double2* buf, int t, Bar bar)
-{
-    bar();  // the warp's previous reads of this single tile are done
-    double2* w = buf + slot_of(t >> 3, t & 7, 0);
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-        w[q] = x[q];
-    bar();
-    const double2* rd = buf + slot_of(t >> 3, 0, t & 7);
-#pragma unroll
-    for (int m = 0; m < 8; m++)
-        x[m] = rd[9 * m];
-}
-template <class Bar>
-__device__ __forceinline__ void exch_p1_to_p0(double2 x[8], double2* buf, int t, Bar bar)
-{
-    double2* w = buf + slot_of(t >> 3, 0, t & 7);
-#pragma unroll
-    for (int m = 0; m < 8; m++)
-        w[9 * m] = x[m];
-    bar();
-    const double2* rd = buf + slot_of(0, t >> 3, t & 7);
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-        x[q] = rd[72 * q];
-}
 
-// Forward transform of the twisted input x (pass-0 layout) -> frequency slots
-// (pass-2 layout).  bufs: two 512-entry double2 tiles (double buffering).
-// bufX: cross-warp exchange tile (needs the 64-thread barrier `bar`);
-// bufW: intra-warp exchange tile (after DIF stage 0 the two 256-point halves are
+// Forward transform of the folded integer input x (pass-0 layout) -> frequency slots
+// (pass-2 layout).  bufX: cross-warp exchange tile (needs the 64-thread barrier `bar`);
+// bufW: intra-warp exchange tile (after tree stage 0 the two 256-point halves are
 // independent and warp w owns half w in passes 1 and 2, so `wbar` = __syncwarp).
 template <class Bar, class WBar>
-__device__ __forceinline__ void fft_forward(double2 x[8], const Twiddles& tw, double2* buf0,
-                                            double2* buf1, int t, Bar bar, WBar wbar)
+__device__ __forceinline__ void fft_forward(double2 x[8], const FwdTw& tw, double2* bufX,
+                                            double2* bufW, int t, Bar bar, WBar wbar)
 {
-    // pass 0: stages 0, 1, 2 (h = 256, 128, 64)
-    dif(x[0], x[4], tw.p0a);
-    dif(x[1], x[5], tw.p0b);
-    dif(x[2], x[6], mul_i(tw.p0a));
-    dif(x[3], x[7], mul_i(tw.p0b));
-    dif(x[0], x[2], tw.p0c);
-    dif(x[1], x[3], mul_i(tw.p0c));
-    dif(x[4], x[6], tw.p0c);
-    dif(x[5], x[7], mul_i(tw.p0c));
-    dif(x[0], x[1], tw.p0d);
-    dif(x[2], x[3], tw.p0d);
-    dif(x[4], x[5], tw.p0d);
-    dif(x[6], x[7], tw.p0d);
-    exch_p0_to_p1(x, buf0, t, bar);
-    // pass 1: stages 3, 4, 5 (h = 32, 16, 8)
-    dif(x[0], x[4], tw.p1a);
-    dif(x[1], x[5], tw.p1b);
-    dif(x[2], x[6], mul_i(tw.p1a));
-    dif(x[3], x[7], mul_i(tw.p1b));
-    dif(x[0], x[2], tw.p1c);
-    dif(x[1], x[3], mul_i(tw.p1c));
-    dif(x[4], x[6], tw.p1c);
-    dif(x[5], x[7], mul_i(tw.p1c));
-    dif(x[0], x[1], tw.p1d);
-    dif(x[2], x[3], tw.p1d);
-    dif(x[4], x[5], tw.p1d);
-    dif(x[6], x[7], tw.p1d);
-    exch_p1_to_p2(x, buf1, t, wbar);
-    // pass 2: stages 6, 7, 8 (h = 4, 2, 1) -- twiddles W[64 q], W[128 (q&1)], W[0]
-    dif_1(x[0], x[4]);
-    dif(x[1], x[5], tw.w64);
-    dif_i(x[2], x[6]);
-    dif(x[3], x[7], mul_i(tw.w64));
-    dif_1(x[0], x[2]);
-    dif_i(x[1], x[3]);
-    dif_1(x[4], x[6]);
-    dif_i(x[5], x[7]);
-    dif_1(x[0], x[1]);
-    dif_1(x[2], x[3]);
-    dif_1(x[4], x[5]);
-    dif_1(x[6], x[7]);
+    fwd_pass0(x);
+    exch_p0_to_p1(x, bufX, t, bar);
+    fwd_pass1(x, tw);
+    exch_p1_to_p2(x, bufW, t, wbar);
+    fwd_pass2(x, tw);
 }
 
-// Inverse transform (unscaled) of frequency slots (pass-2 layout) -> natural order
-// (pass-0 layout).  The 1/M scale lives in the untwist table.
+// Inverse transform (unscaled, no untwist) of frequency slots (pass-2 layout) ->
+// natural order (pass-0 layout), for one polynomial.
 template <class Bar, class WBar>
-__device__ __forceinline__ void fft_inverse(double2 x[8], const Twiddles& tw, double2* buf0,
-                                            double2* buf1, int t, Bar bar, WBar wbar)
+__device__ __forceinline__ void fft_inverse(double2 x[8], const InvTw& tw, double2* bufX,
+                                            double2* bufW, int t, Bar bar, WBar wbar)
 {
-    // pass 2^-1: stages 8, 7, 6
-    dit_1(x[0], x[1]);
-    dit_1(x[2], x[3]);
-    dit_1(x[4], x[5]);
-    dit_1(x[6], x[7]);
-    dit_1(x[0], x[2]);
-    dit_mi(x[1], x[3]);
-    dit_1(x[4], x[6]);
-    dit_mi(x[5], x[7]);
-    dit_1(x[0], x[4]);
-    dit(x[1], x[5], conj2(tw.w64));
-    dit_mi(x[2], x[6]);
-    dit(x[3], x[7], conj2(mul_i(tw.w64)));
-    exch_p2_to_p1(x, buf1, t, wbar);
-    // pass 1^-1: stages 5, 4, 3
-    dit(x[0], x[1], conj2(tw.p1d));
-    dit(x[2], x[3], conj2(tw.p1d));
-    dit(x[4], x[5], conj2(tw.p1d));
-    dit(x[6], x[7], conj2(tw.p1d));
-    dit(x[0], x[2], conj2(tw.p1c));
-    dit(x[1], x[3], conj2(mul_i(tw.p1c)));
-    dit(x[4], x[6], conj2(tw.p1c));
-    dit(x[5], x[7], conj2(mul_i(tw.p1c)));
-    dit(x[0], x[4], conj2(tw.p1a));
-    dit(x[1], x[5], conj2(tw.p1b));
-    dit(x[2], x[6], conj2(mul_i(tw.p1a)));
-    dit(x[3], x[7], conj2(mul_i(tw.p1b)));
-    exch_p1_to_p0(x, buf0, t, bar);
-    // pass 0^-1: stages 2, 1, 0
-    dit(x[0], x[1], conj2(tw.p0d));
-    dit(x[2], x[3], conj2(tw.p0d));
-    dit(x[4], x[5], conj2(tw.p0d));
-    dit(x[6], x[7], conj2(tw.p0d));
-    dit(x[0], x[2], conj2(tw.p0c));
-    dit(x[1], x[3], conj2(mul_i(tw.p0c)));
-    dit(x[4], x[6], conj2(tw.p0c));
-    dit(x[5], x[7], conj2(mul_i(tw.p0c)));
-    dit(x[0], x[4], conj2(tw.p0a));
-    dit(x[1], x[5], conj2(tw.p0b));
-    dit(x[2], x[6], conj2(mul_i(tw.p0a)));
-    dit(x[3], x[7], conj2(mul_i(tw.p0b)));
-}
-
-// ---- paired transforms: two independent polynomials per thread in lockstep; they share
-// every exchange barrier and the compiler interleaves their butterflies (2x ILP).  The
-// per-polynomial arithmetic is exactly fft_forward / fft_inverse.
-__device__ __forceinline__ void pass0_fwd(double2 x[8], const Twiddles& tw)
-{
-    dif(x[0], x[4], tw.p0a);
-    dif(x[1], x[5], tw.p0b);
-    dif(x[2], x[6], mul_i(tw.p0a));
-    dif(x[3], x[7], mul_i(tw.p0b));
-    dif(x[0], x[2], tw.p0c);
-    dif(x[1], x[3], mul_i(tw.p0c));
-    dif(x[4], x[6], tw.p0c);
-    dif(x[5], x[7], mul_i(tw.p0c));
-    dif(x[0], x[1], tw.p0d);
-    dif(x[2], x[3], tw.p0d);
-    dif(x[4], x[5], tw.p0d);
-    dif(x[6], x[7], tw.p0d);
-}
-__device__ __forceinline__ void pass1_fwd(double2 x[8], const Twiddles& tw)
-{
-    dif(x[0], x[4], tw.p1a);
-    dif(x[1], x[5], tw.p1b);
-    dif(x[2], x[6], mul_i(tw.p1a));
-    dif(x[3], x[7], mul_i(tw.p1b));
-    dif(x[0], x[2], tw.p1c);
-    dif(x[1], x[3], mul_i(tw.p1c));
-    dif(x[4], x[6], tw.p1c);
-    dif(x[5], x[7], mul_i(tw.p1c));
-    dif(x[0], x[1], tw.p1d);
-    dif(x[2], x[3], tw.p1d);
-    dif(x[4], x[5], tw.p1d);
-    dif(x[6], x[7], tw.p1d);
-}
-__device__ __forceinline__ void pass2_fwd(double2 x[8], const Twiddles& tw)
-{
-    dif_1(x[0], x[4]);
-    dif(x[1], x[5], tw.w64);
-    dif_i(x[2], x[6]);
-    dif(x[3], x[7], mul_i(tw.w64));
-    dif_1(x[0], x[2]);
-    dif_i(x[1], x[3]);
-    dif_1(x[4], x[6]);
-    dif_i(x[5], x[7]);
-    dif_1(x[0], x[1]);
-    dif_1(x[2], x[3]);
-    dif_1(x[4], x[5]);
-    dif_1(x[6], x[7]);
-}
-__device__ __forceinline__ void pass2_inv(double2 x[8], const Twiddles& tw)
-{
-    dit_1(x[0], x[1]);
-    dit_1(x[2], x[3]);
-    dit_1(x[4], x[5]);
-    dit_1(x[6], x[7]);
-    dit_1(x[0], x[2]);
-    dit_mi(x[1], x[3]);
-    dit_1(x[4], x[6]);
-    dit_mi(x[5], x[7]);
-    dit_1(x[0], x[4]);
-    dit(x[1], x[5], conj2(tw.w64));
-    dit_mi(x[2], x[6]);
-    dit(x[3], x[7], conj2(mul_i(tw.w64)));
-}
-__device__ __forceinline__ void pass1_inv(double2 x[8], const Twiddles& tw)
-{
-    dit(x[0], x[1], conj2(tw.p1d));
-    dit(x[2], x[3], conj2(tw.p1d));
-    dit(x[4], x[5], conj2(tw.p1d));
-    dit(x[6], x[7], conj2(tw.p1d));
-    dit(x[0], x[2], conj2(tw.p1c));
-    dit(x[1], x[3], conj2(mul_i(tw.p1c)));
-    dit(x[4], x[6], conj2(tw.p1c));
-    dit(x[5], x[7], conj2(mul_i(tw.p1c)));
-    dit(x[0], x[4], conj2(tw.p1a));
-    dit(x[1], x[5], conj2(tw.p1b));
-    dit(x[2], x[6], conj2(mul_i(tw.p1a)));
-    dit(x[3], x[7], conj2(mul_i(tw.p1b)));
-}
-__device__ __forceinline__ void pass0_inv(double2 x[8], const Twiddles& tw)
-{
-    dit(x[0], x[1], conj2(tw.p0d));
-    dit(x[2], x[3], conj2(tw.p0d));
-    dit(x[4], x[5], conj2(tw.p0d));
-    dit(x[6], x[7], conj2(tw.p0d));
-    dit(x[0], x[2], conj2(tw.p0c));
-    dit(x[1], x[3], conj2(mul_i(tw.p0c)));
-    dit(x[4], x[6], conj2(tw.p0c));
-    dit(x[5], x[7], conj2(mul_i(tw.p0c)));
-    dit(x[0], x[4], conj2(tw.p0a));
-    dit(x[1], x[5], conj2(tw.p0b));
-    dit(x[2], x[6], conj2(mul_i(tw.p0a)));
-    dit(x[3], x[7], conj2(mul_i(tw.p0b)));
-}
-
-// cross tiles c0/c1 are single-buffered: the leading barrier orders this write after
-// every thread's previous read of the same tile.
-template <class Bar, class WBar>
-__device__ __forceinline__ void fft_forward2(double2 x0[8], double2 x1[8], const Twiddles& tw,
-                                             double2* c0, double2* c1, double2* w0, double2* w1,
-                                             int t, Bar bar, WBar wbar)
-{
-    pass0_fwd(x0, tw);
-    pass0_fwd(x1, tw);
-    bar();
+    inv_pass2(x);
     {
-        double2* a = c0 + slot_of(0, t >> 3, t & 7);
-        double2* b = c1 + slot_of(0, t >> 3, t & 7);
+        wbar();
+        double2* w = bufW + slot_of(t >> 3, t & 7, 0);
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-            a[72 * q] = x0[q];
-            b[72 * q] = x1[q];
-        }
+        for (int q = 0; q < 8; q++)
+            w[q] = x[q];
+        wbar();
+        const double2* rd = bufW + slot_of(t >> 3, 0, t & 7);
+#pragma unroll
+        for (int m = 0; m < 8; m++)
+            x[m] = rd[9 * m];
+    }
+    inv_pass1(x, tw);
+    {
         bar();
-        const double2* ra = c0 + slot_of(t >> 3, 0, t & 7);
-        const double2* rb = c1 + slot_of(t >> 3, 0, t & 7);
+        double2* w = bufX + slot_of(t >> 3, 0, t & 7);
 #pragma unroll
-        for (int m = 0; m < 8; m++) {
-            x0[m] = ra[9 * m];
-            x1[m] = rb[9 * m];
-        }
+        for (int m = 0; m < 8; m++)
+            w[9 * m] = x[m];
+        bar();
+        const double2* rd = bufX + slot_of(0, t >> 3, t & 7);
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            x[q] = rd[72 * q];
     }
-    pass1_fwd(x0, tw);
-    pass1_fwd(x1, tw);
-    {
-        wbar();
-        double2* a = w0 + slot_of(t >> 3, 0, t & 7);
-        double2* b = w1 + slot_of(t >> 3, 0, t & 7);
-#pragma unroll
-        for (int m = 0; m < 8; m++) {
-            a[9 * m] = x0[m];
-            b[9 * m] = x1[m];
-        }
-        wbar();
-        const double2* ra = w0 + slot_of(t >> 3, t & 7, 0);
-        const double2* rb = w1 + slot_of(t >> 3, t & 7, 0);
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            x0[q] = ra[q];
-            x1[q] = rb[q];
-        }
-    }
-    pass2_fwd(x0, tw);
-    pass2_fwd(x1, tw);
+    inv_pass0(x, tw);
 }
 
+// Two inverse transforms in lockstep (outputs A and B of one external product): they
+// share every exchange barrier and the compiler interleaves their butterflies.
+// c0/c1 cross tiles, w0/w1 intra tiles (may alias c0/c1: a CTA barrier separates uses).
 template <class Bar, class WBar>
-__device__ __forceinline__ void fft_inverse2(double2 x0[8], double2 x1[8], const Twiddles& tw,
+__device__ __forceinline__ void fft_inverse2(double2 x0[8], double2 x1[8], const InvTw& tw,
                                              double2* c0, double2* c1, double2* w0, double2* w1,
                                              int t, Bar bar, WBar wbar)
 {
-    pass2_inv(x0, tw);
-    pass2_inv(x1, tw);
+    inv_pass2(x0);
+    inv_pass2(x1);
     {
         wbar();
         double2* a = w0 + slot_of(t >> 3, t & 7, 0);
@@ -439,8 +345,8 @@ __device__ __forceinline__ void fft_inverse2(double2 x0[8], double2 x1[8], const
             x1[m] = rb[9 * m];
         }
     }
-    pass1_inv(x0, tw);
-    pass1_inv(x1, tw);
+    inv_pass1(x0, tw);
+    inv_pass1(x1, tw);
     bar();
     {
         double2* a = c0 + slot_of(t >> 3, 0, t & 7);
@@ -459,8 +365,8 @@ __device__ __forceinline__ void fft_inverse2(double2 x0[8], double2 x1[8], const
             x1[q] = rb[72 * q];
         }
     }
-    pass0_inv(x0, tw);
-    pass0_inv(x1, tw);
+    inv_pass0(x0, tw);
+    inv_pass0(x1, tw);
 }
 
 }  // namespace lpb

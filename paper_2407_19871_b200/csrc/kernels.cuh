@@ -54,26 +54,36 @@ struct DevParams {
     uint32_t N_stride;  // padded N+1
 };
 
+// The transform's device tables (engine.cu make_tables; same values as the oracle's
+// or_fft2_make_tables): per-thread forward / inverse twiddles [8][64] and the factored
+// twist psi^j (the untwist is its conjugate).
+struct FftTabs {
+    const double2* fwd;
+    const double2* inv;
+    const double2* tw;
+};
+__constant__ double2 c_twq[8];  // psi^(64 q), q = 0..7: psi^(t + 64 q) = cmul(psi^t, psi^(64 q))
+
+// untwist factor conj(psi^(t + 64 q)) from the thread's psi^t
+__device__ __forceinline__ double2 untwist(double2 twt, int q) { return conj2(cmul(twt, c_twq[q])); }
+
 // ---------------------------------------------------------------------------
-// K0: BK torus polynomials -> frequency domain, layout [poly][q*64 + t] where the
-// frequency slot is 8t + q (so K1's per-thread loads are coalesced).
+// K0: BK torus polynomials -> frequency domain (scaled by 1/512, exact), layout
+// [poly][q*64 + t] where the frequency slot is 8t + q (K1's per-thread loads coalesce).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ bk,
-                                                   double2* __restrict__ out,
-                                                   const double2* __restrict__ W,
-                                                   const double2* __restrict__ TW)
+                                                   double2* __restrict__ out, FftTabs tb)
 {
     __shared__ __align__(16) double2 xbuf[2][XTILE];
     const int t = threadIdx.x;
     const size_t poly = blockIdx.x;
     const uint32_t* b = bk + poly * 1024;
-    const Twiddles tw = load_twiddles(W, t);
+    const FwdTw tw = load_fwd_tw(tb.fwd, t);
     double2 x[8];
 #pragma unroll
     for (int q = 0; q < 8; q++) {
         const int j = t + 64 * q;
-        const double2 a = make_double2((double)(int32_t)b[j], (double)(int32_t)b[j + 512]);
-        x[q] = cmul(a, TW[j]);
+        x[q] = make_double2((double)(int32_t)b[j], (double)(int32_t)b[j + 512]);
     }
     auto bar = [] { __syncthreads(); };
     auto wbar = [] { __syncwarp(); };
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
     double2* o = out + poly * FFT_M;
 #pragma unroll
     for (int q = 0; q < 8; q++)
-        o[q * 64 + t] = x[q];
+        o[q * 64 + t] = make_double2(x[q].x * (1.0 / 512.0), x[q].y * (1.0 / 512.0));
 }
 
 // ---------------------------------------------------------------------------
@@ -92,36 +102,6 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
 // MAX_N + 1 entries.
 constexpr int MAX_N = 639;
 constexpr uint32_t MAX_CTX_N = 636;
-#ifndef TWIST_REGS
-#define TWIST_REGS 0
-#endif
-// TWIST_CONST: twist factor psi^(t + 64 q) = cmul(psi^t, psi^(64 q)) formed on the fly from
-// a per-thread register and a __constant__ table (trades shared-memory reads for FP64)
-#ifndef TWIST_CONST
-#define TWIST_CONST 1
-#endif
-#ifndef BK_EVICT_LAST
-#define BK_EVICT_LAST 1
-#endif
-#ifndef TWIST_TMEM
-#define TWIST_TMEM 0
-#endif
-#ifndef BK_RELAXED
-#define BK_RELAXED 1
-#endif
-#ifndef BK_PREFETCH
-#define BK_PREFETCH 2
-#endif
-#ifndef LAT_TMA
-#define LAT_TMA 0
-#endif
-#ifndef INV_PAIR
-#define INV_PAIR 1
-#endif
-#ifndef BR_PUNROLL
-#define BR_PUNROLL 1
-#endif
-constexpr int kPUnroll = BR_PUNROLL;  // digit-row loop unrolling in K1
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4
 #endif
@@ -134,122 +114,19 @@ __device__ __forceinline__ uint32_t rot_read(const uint32_t* p, uint32_t a, int 
     return idx < 1024u ? v : 0u - v;
 }
 
-// ---- TMEM (tcgen05) as per-thread scratch for the frequency-domain accumulators.
-// Each thread owns one TMEM lane (warp w -> lanes 32w..32w+31); columns [0,32) hold
-// OUT_A, [32,64) OUT_B, as 8 complex doubles (re lo/hi, im lo/hi) each.
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t (&v)[32])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
-
-__device__ __forceinline__ void tmem_st32(uint32_t addr, const uint32_t (&v)[32])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n"
-        :
-        : "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
-          "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
-          "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]),
-          "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]),
-          "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15}, [%16];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15])
-        : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
-
-__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15,%16};\n"
-        :
-        : "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
-          "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
-          "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-
-__device__ __forceinline__ double2 unpack2(const uint32_t* v)
-{
-    return make_double2(__hiloint2double((int)v[1], (int)v[0]), __hiloint2double((int)v[3], (int)v[2]));
-}
-__device__ __forceinline__ void pack2(uint32_t* v, double2 d)
-{
-    v[0] = (uint32_t)__double2loint(d.x);
-    v[1] = (uint32_t)__double2hiint(d.x);
-    v[2] = (uint32_t)__double2loint(d.y);
-    v[3] = (uint32_t)__double2hiint(d.y);
-}
-
-// UT[j] = conj(TW[j]) / 512: scaling by a power of two is exact, so this equals the
-// oracle's untwist table bit for bit.
-__device__ __forceinline__ double2 untwist(double2 tw)
-{
-    return make_double2(tw.x * (1.0 / 512.0), -tw.y * (1.0 / 512.0));
-}
-
-// BK is streamed once per CTA per step: keep it out of L1 (it stays in L2).
+// BK rows are streamed once per CTA per step: kept out of L1 and pinned in L2
+// (evict_last).  A relaxed gpu-scope load may not be sunk below the transform's
+// bar.sync by ptxas (a weak .nc load is, which turns the prefetch into a stall at the MAC).
 __device__ __forceinline__ double2 ld_stream(const double2* p)
 {
     double2 v;
-#if BK_RELAXED
-    // a relaxed gpu-scope load may not be sunk below the FFT's bar.sync by ptxas (a weak
-    // .nc load is, which turns the prefetch into a stall at the MAC)
     asm volatile(
         "{\n\t.reg .b64 pol;\n\t"
         "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
         "ld.relaxed.gpu.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
         : "=d"(v.x), "=d"(v.y)
         : "l"(p));
-#elif BK_EVICT_LAST
-    asm volatile(
-        "{\n\t.reg .b64 pol;\n\t"
-        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-        "ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
-        : "=d"(v.x), "=d"(v.y)
-        : "l"(p));
-#else
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
-                 : "=d"(v.x), "=d"(v.y)
-                 : "l"(p));
-#endif
     return v;
-}
-
-#ifndef I2F_MAGIC
-#define I2F_MAGIC 0
-#endif
-// int -> double for |d| < 2^31: exact either way; the magic-number form trades the
-// conversion instruction for one integer op and one DADD.
-__device__ __forceinline__ double i2d(int d)
-{
-#if I2F_MAGIC
-    return __dsub_rn(__hiloint2double(0x43300000, (uint32_t)d ^ 0x80000000u), 4503601774854144.0);
-#else
-    return (double)d;
-#endif
 }
 
 __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
@@ -262,77 +139,13 @@ __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
     acc.y = im;
 }
 
-__constant__ double2 c_twq[8];  // psi^(64 q), q = 0..7 (TWIST_CONST)
-
-#ifndef BK_TMA
-#define BK_TMA 0
-#endif
-// ACC_TMEM (opt-in): frequency-domain accumulators in TMEM (64 columns per CTA) and BK
-// loaded at MAC time, to fit 168 registers = 6 CTAs (12 warps) per SM.
-#ifndef ACC_TMEM
-#define ACC_TMEM 0
-#endif
-constexpr size_t BR_DYN_SMEM = BK_TMA ? 2 * FFT_M * sizeof(double2) : 0;
-// BK_TMA (opt-in): each CTA streams its BK rows with bulk async copies (TMA engine) into
-// a 16 KB shared-memory row buffer, completion tracked by an mbarrier.
-__device__ __forceinline__ uint32_t smem_u32(const void* p)
-{
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
-{
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "{\n\t.reg .b64 pol;\n\t"
-        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], pol;\n\t}\n" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
-{
-    asm volatile(
-        "{\n\t.reg .b64 pol;\n\t"
-        "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], pol;\n\t}\n" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
-{
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-
 // ERR = true (diagnostic instantiation only): also record max |w - rint(w)| over every
 // inverse-transform output before rounding -- the FFT rounding margin (exact iff < 1/2).
 template <int L, int BGBIT, bool ERR = false>
 __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     k_blind_rotate(DevParams dp, const BrItem* __restrict__ items,
                    const uint32_t* __restrict__ pool_n, uint32_t* __restrict__ pool_N,
-                   const double2* __restrict__ bkf, const double2* __restrict__ W,
-                   const double2* __restrict__ TW, const double2* __restrict__ UT, uint32_t mu,
+                   const double2* __restrict__ bkf, FftTabs tb, uint32_t mu,
                    unsigned long long* err_out = nullptr)
 {
     double emax = 0.0;
@@ -340,63 +153,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     // exchange tiles: [0],[1] cross-warp (alternating), [2] intra-warp
     __shared__ __align__(16) double2 xbuf[3][XTILE];
     __shared__ uint16_t abar[MAX_N + 1];
-#if !TWIST_REGS && !TWIST_TMEM && !TWIST_CONST
-    __shared__ __align__(16) double2 tws[FFT_M];  // twist table psi^j
-#endif
-#if TWIST_TMEM
-    __shared__ uint32_t tmem_slot;
-#endif
 
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
-#if BK_TMA
-    extern __shared__ __align__(128) double2 bkrow[];  // [2][FFT_M]: one BK row, both outputs
-    __shared__ __align__(8) uint64_t bkbar;
-#endif
-#if ACC_TMEM
-    __shared__ uint32_t acc_tslot;
-    if (t < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&acc_tslot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    const uint32_t tacc = acc_tslot + ((uint32_t)(t & 32) << 16);  // this warp's lane quarter
-#endif
-#if TWIST_TMEM
-    if (t < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    const uint32_t ttw = tmem_slot + ((uint32_t)(t & 32) << 16);
-    {
-        uint32_t v[32];
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-            pack2(v + 4 * q, TW[t + 64 * q]);
-        tmem_st32(ttw, v);
-        tmem_wait_st();
-    }
-#elif TWIST_CONST
-    const double2 twt = TW[t];
-#define TWIST(q) cmul(twt, c_twq[q])
-#elif TWIST_REGS
-    double2 twr[8];  // this thread's twist factors psi^j, j = t + 64 q (untwist = conj / 512)
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-        twr[q] = TW[t + 64 * q];
-#define TWIST(q) twr[q]
-#else
-    for (int j = t; j < FFT_M; j += 64)
-        tws[j] = TW[j];
-#define TWIST(q) tws[t + 64 * (q)]
-#endif
     const uint32_t n = dp.n;
 
     // ---- prologue: gate linear form (gate_engine.hpp:196-269) + mod switch to [0, 2N)
@@ -425,43 +184,11 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j] = idx < 1024u ? mu : 0u - mu;
         }
     }
-    const Twiddles tw = load_twiddles(W, t);
+    const FwdTw tw = load_fwd_tw(tb.fwd, t);
+    const double2 twt = tb.tw[t];  // psi^t (untwist factors formed on the fly)
     auto bar = [] { __syncthreads(); };
     auto wbar = [] { __syncwarp(); };
     int xs = 0;  // alternating cross-warp tile
-#if BK_TMA
-    constexpr uint32_t ROW_BYTES = 2 * FFT_M * sizeof(double2);
-    // the row consumed next: (step, row) -- steps with abar = 0 are skipped
-    auto issue_row = [&](uint32_t step, int row) {
-        while (step < n && abar[step] == 0)
-            step++;
-        if (step < n)
-            tma_load_row(bkrow, bkf + ((size_t)step * (2 * L) + row) * 2 * FFT_M, ROW_BYTES, &bkbar);
-    };
-    uint32_t bkphase = 0;
-    if (t == 0)
-        mbar_init(&bkbar, 1);
-    __syncthreads();
-    if (t == 0)
-        issue_row(0, 0);
-#if BK_TMA == 2
-    // refill issued at the next transform's first CTA barrier (no extra barrier)
-    uint32_t pend_step = 0xFFFFFFFFu;
-    int pend_row = 0;
-    auto bar_tma = [&] {
-        __syncthreads();
-        if (t == 0 && pend_step != 0xFFFFFFFFu) {
-            issue_row(pend_step, pend_row);
-            pend_step = 0xFFFFFFFFu;
-        }
-    };
-#endif
-#endif
-#if BK_TMA == 2
-#define FFT_BAR bar_tma
-#else
-#define FFT_BAR bar
-#endif
 
     constexpr uint32_t HALF = 1u << (BGBIT - 1);
     constexpr uint32_t MASK = (1u << BGBIT) - 1;
@@ -477,16 +204,12 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         const uint32_t a = abar[i];
         if (a == 0)
             continue;
-#if ACC_TMEM
-        bool first = true;
-#else
         double2 oA[8], oB[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             oA[q] = make_double2(0.0, 0.0);
             oB[q] = make_double2(0.0, 0.0);
         }
-#endif
         const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
 #pragma unroll
         for (int c = 0; c < 2; c++) {
@@ -497,117 +220,44 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 tmp[q] = rot_read(acc[c], a, j) - acc[c][j] + OFF;
                 tmp[8 + q] = rot_read(acc[c], a, j + 512) - acc[c][j + 512] + OFF;
             }
-#pragma unroll kPUnroll
+#pragma unroll 1
             for (int p = 0; p < L; p++) {
-                // prefetch this row's BK slots; the loads land while the FFT runs
+                // prefetch this row's BK slots; the loads land while the transform runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
-#if !BK_TMA && !ACC_TMEM
                 double2 BA[8], BB[8];
-#endif
-#if !BK_TMA && !ACC_TMEM && BK_PREFETCH >= 1
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BA[q] = ld_stream(row + q * 64 + t);
-#endif
-#if !BK_TMA && !ACC_TMEM && BK_PREFETCH >= 2
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
-#endif
-                (void)row;
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
-#if TWIST_TMEM
-                uint32_t tv[32];
-                tmem_ld32(ttw, tv);
-#define TWIST(q) unpack2(tv + 4 * (q))
-#endif
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     const int dlo = (int)((tmp[q] >> sh) & MASK) - (int)HALF;
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
-                    x[q] = cmul(make_double2(i2d(dlo), i2d(dhi)), TWIST(q));
+                    x[q] = make_double2((double)dlo, (double)dhi);
                 }
-#if TWIST_TMEM
-#undef TWIST
-#endif
-                fft_forward(x, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
+                fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
-#if ACC_TMEM
-                // MAC into the TMEM accumulators, 4 slots at a time; BK loaded here
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    uint32_t va[16], vb[16];
-                    if (!first) {
-                        tmem_ld16(tacc + 16 * h, va);
-                        tmem_ld16(tacc + 32 + 16 * h, vb);
-                    }
-#pragma unroll
-                    for (int qq = 0; qq < 4; qq++) {
-                        const int q = 4 * h + qq;
-                        double2 oa = first ? make_double2(0.0, 0.0) : unpack2(va + 4 * qq);
-                        double2 ob = first ? make_double2(0.0, 0.0) : unpack2(vb + 4 * qq);
-                        mac(oa, x[q], ld_stream(row + q * 64 + t));
-                        mac(ob, x[q], ld_stream(row + FFT_M + q * 64 + t));
-                        pack2(va + 4 * qq, oa);
-                        pack2(vb + 4 * qq, ob);
-                    }
-                    tmem_st16(tacc + 16 * h, va);
-                    tmem_st16(tacc + 32 + 16 * h, vb);
-                }
-                tmem_wait_st();
-                first = false;
-#elif BK_TMA
-                mbar_wait(&bkbar, bkphase);
-                bkphase ^= 1u;
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    mac(oA[q], x[q], bkrow[q * 64 + t]);
-                    mac(oB[q], x[q], bkrow[FFT_M + q * 64 + t]);
-                }
-#if BK_TMA == 2
-                if (t == 0) {  // refill at the next CTA barrier (every thread is past this MAC)
-                    const int rw = c * L + p;
-                    pend_step = rw + 1 < 2 * L ? i : i + 1;
-                    pend_row = rw + 1 < 2 * L ? rw + 1 : 0;
-                }
-#else
-                __syncthreads();  // row buffer free: refill it with the next row
-                if (t == 0) {
-                    const int rw = c * L + p;
-                    if (rw + 1 < 2 * L)
-                        issue_row(i, rw + 1);
-                    else
-                        issue_row(i + 1, 0);
-                }
-#endif
-#else
-#if BK_PREFETCH < 2
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
-#endif
-#if BK_PREFETCH < 1
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BA[q] = ld_stream(row + q * 64 + t);
-#endif
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     mac(oA[q], x[q], BA[q]);
                     mac(oB[q], x[q], BB[q]);
                 }
-#endif
             }
         }
-#if INV_PAIR && !ACC_TMEM && !TWIST_TMEM
         // both inverse transforms in lockstep: shared barriers, twice the ILP.  Tiles:
         // intra and cross exchanges alias xbuf[2] / xbuf[xs] (a CTA barrier separates them)
-        fft_inverse2(oA, oB, tw, xbuf[2], xbuf[xs], xbuf[2], xbuf[xs], t, FFT_BAR, wbar);
+        {
+            const InvTw itw = load_inv_tw(tb.inv, t);
+            fft_inverse2(oA, oB, itw, xbuf[2], xbuf[xs], xbuf[2], xbuf[xs], t, bar, wbar);
+        }
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int j = t + 64 * q;
-            const double2 ut = untwist(TWIST(q));
+            const double2 ut = untwist(twt, q);
             const double2 wa = cmul(oA[q], ut);
             const double2 wb = cmul(oB[q], ut);
             if constexpr (ERR)
@@ -618,64 +268,8 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j] += (uint32_t)__double2ll_rn(wb.x);
             acc[1][j + 512] += (uint32_t)__double2ll_rn(wb.y);
         }
-#else
-        // inverse transforms, round, accumulate into ACC
-#if ACC_TMEM
-        double2 oA[8], oB[8];
-        {
-            uint32_t v[32];
-            tmem_ld32(tacc, v);
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                oA[q] = unpack2(v + 4 * q);
-        }
-#endif
-        fft_inverse(oA, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
-        xs ^= 1;
-#if TWIST_TMEM
-        uint32_t tv[32];
-        tmem_ld32(ttw, tv);
-#define TWIST(q) unpack2(tv + 4 * (q))
-#endif
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const int j = t + 64 * q;
-            const double2 w = cmul(oA[q], untwist(TWIST(q)));
-            if constexpr (ERR)
-                emax = fmax(emax, fmax(fabs(w.x - rint(w.x)), fabs(w.y - rint(w.y))));
-            acc[0][j] += (uint32_t)__double2ll_rn(w.x);
-            acc[0][j + 512] += (uint32_t)__double2ll_rn(w.y);
-        }
-#if ACC_TMEM
-        {
-            uint32_t v[32];
-            tmem_ld32(tacc + 32, v);
-#pragma unroll
-            for (int q = 0; q < 8; q++)
-                oB[q] = unpack2(v + 4 * q);
-        }
-#endif
-        fft_inverse(oB, tw, xbuf[xs], xbuf[2], t, FFT_BAR, wbar);
-        xs ^= 1;
-#if TWIST_TMEM
-        tmem_ld32(ttw, tv);
-#endif
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const int j = t + 64 * q;
-            const double2 w = cmul(oB[q], untwist(TWIST(q)));
-            if constexpr (ERR)
-                emax = fmax(emax, fmax(fabs(w.x - rint(w.x)), fabs(w.y - rint(w.y))));
-            acc[1][j] += (uint32_t)__double2ll_rn(w.x);
-            acc[1][j + 512] += (uint32_t)__double2ll_rn(w.y);
-        }
-#endif
-#if TWIST_TMEM
-#undef TWIST
-#endif
     }
     __syncthreads();
-#undef FFT_BAR
     // ---- sample extraction at index 0 (N-dim LWE under the TRLWE key)
     uint32_t* o = pool_N + (size_t)it.out * dp.N_stride;
     for (int j = t; j < 1024; j += 64)
@@ -684,20 +278,6 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         o[1024] = acc[1][0];
     if constexpr (ERR)  // positive doubles order like their bit patterns
         atomicMax(err_out, (unsigned long long)__double_as_longlong(emax));
-#if ACC_TMEM
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (t < 32)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(acc_tslot));
-#endif
-#if TWIST_TMEM
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (t < 32)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem_slot));
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1064,23 +644,13 @@ __global__ void __launch_bounds__(KS_THREADS)
 template <int L>
 struct LatSmem {
     uint32_t acc[2][1024];
-    double2 tws[FFT_M];
     double2 F[2 * L][FFT_M];              // digit spectra, slot layout [q*64 + t]
     double2 O[2][FFT_M];                  // MAC results per output component
     double2 tiles[2 * L][2][XTILE];       // per group: cross-warp tile, intra-warp tile
     uint16_t abar[MAX_N + 1];
 };
-// 80-bit (L = 2): the whole BK_i (64 KB) also fits, streamed one step ahead by TMA
 template <int L>
-struct LatSmemBk {
-    LatSmem<L> s;
-    __align__(128) double2 bk[2 * L][2][FFT_M];
-    __align__(8) uint64_t bar;
-};
-template <int L>
-constexpr bool kLatTma = LAT_TMA && L == 2;
-template <int L>
-constexpr size_t kLatSmemBytes = kLatTma<L> ? sizeof(LatSmemBk<L>) : sizeof(LatSmem<L>);
+constexpr size_t kLatSmemBytes = sizeof(LatSmem<L>);
 
 __device__ __forceinline__ void group_bar(int id)
 {
@@ -1091,16 +661,13 @@ template <int L, int BGBIT>
 __global__ void __launch_bounds__(128 * L, 1)
     k_blind_rotate_lat(DevParams dp, const BrItem* __restrict__ items,
                        const uint32_t* __restrict__ pool_n, uint32_t* __restrict__ pool_N,
-                       const double2* __restrict__ bkf, const double2* __restrict__ W,
-                       const double2* __restrict__ TW, uint32_t mu)
+                       const double2* __restrict__ bkf, FftTabs tb, uint32_t mu)
 {
     extern __shared__ __align__(16) uint8_t smem_l[];
     LatSmem<L>& S = *reinterpret_cast<LatSmem<L>*>(smem_l);
     const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
     const BrItem it = items[blockIdx.x];
     const uint32_t n = dp.n;
-    for (int j = threadIdx.x; j < FFT_M; j += blockDim.x)
-        S.tws[j] = TW[j];
     {
         const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
         const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
@@ -1117,33 +684,6 @@ __global__ void __launch_bounds__(128 * L, 1)
         }
     }
     __syncthreads();
-    constexpr int ROWS_ = 2 * L;
-    [[maybe_unused]] uint32_t bkphase = 0;
-    [[maybe_unused]] auto issue_bk = [&](uint32_t step) {
-        if constexpr (kLatTma<L>) {
-            LatSmemBk<L>& SB = *reinterpret_cast<LatSmemBk<L>*>(smem_l);
-            while (step < n && S.abar[step] == 0)
-                step++;
-            if (step < n) {
-                constexpr uint32_t BYTES = ROWS_ * 2 * FFT_M * sizeof(double2);
-                const double2* src = bkf + (size_t)step * ROWS_ * 2 * FFT_M;
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                mbar_expect_tx(&SB.bar, BYTES);
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    bulk_copy(&SB.bk[0][0][0] + (size_t)k * (BYTES / 64), src + (size_t)k * (BYTES / 64),
-                              BYTES / 4, &SB.bar);
-            }
-        }
-    };
-    if constexpr (kLatTma<L>) {
-        LatSmemBk<L>& SB = *reinterpret_cast<LatSmemBk<L>*>(smem_l);
-        if (threadIdx.x == 0)
-            mbar_init(&SB.bar, 1);
-        __syncthreads();
-        if (threadIdx.x == 0)
-            issue_bk(0);
-    }
     {
         const uint32_t e = (2048u - S.abar[n]) & 2047u;
         for (int j = threadIdx.x; j < 1024; j += blockDim.x) {
@@ -1152,7 +692,8 @@ __global__ void __launch_bounds__(128 * L, 1)
             S.acc[1][j] = idx < 1024u ? mu : 0u - mu;
         }
     }
-    const Twiddles tw = load_twiddles(W, t);
+    const FwdTw ftw = load_fwd_tw(tb.fwd, t);
+    const double2 twt = tb.tw[t];
     const int bid = 1 + g;
     auto bar = [bid] { group_bar(bid); };
     auto wbar = [] { __syncwarp(); };
@@ -1179,7 +720,7 @@ __global__ void __launch_bounds__(128 * L, 1)
             continue;
         // this thread's BK values for its MAC slots, in flight during the transform
         double2 bkv[ROWS][P];
-        if constexpr (!kLatTma<L>) {
+        {
             const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M + (size_t)mcomp * FFT_M;
 #pragma unroll
             for (int r = 0; r < ROWS; r++)
@@ -1187,11 +728,7 @@ __global__ void __launch_bounds__(128 * L, 1)
                 for (int k = 0; k < P; k++) {
                     const int q = msub + L * k;
                     if (q < 8)
-#if LAT_SKIP_BK
-                        bkv[r][k] = make_double2(1.0 + r, 0.5 * k);
-#else
                         bkv[r][k] = ld_stream(bki + (size_t)r * 2 * FFT_M + q * 64 + t);
-#endif
                 }
         }
         // every group: digit (c, p) of (X^a - 1) ACC_c -> forward transform -> F[g]
@@ -1204,49 +741,26 @@ __global__ void __launch_bounds__(128 * L, 1)
                 const uint32_t hi = rot_read(S.acc[c], a, j + 512) - S.acc[c][j + 512] + OFF;
                 const int dlo = (int)((lo >> sh) & MASK) - (int)HALF;
                 const int dhi = (int)((hi >> sh) & MASK) - (int)HALF;
-                x[q] = cmul(make_double2((double)dlo, (double)dhi), S.tws[j]);
+                x[q] = make_double2((double)dlo, (double)dhi);
             }
-#if !LAT_SKIP_FWD
-            fft_forward(x, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
-#endif
+            fft_forward(x, ftw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 S.F[g][q * 64 + t] = x[q];
         }
         __syncthreads();
-        if constexpr (kLatTma<L>) {
-            LatSmemBk<L>& SB = *reinterpret_cast<LatSmemBk<L>*>(smem_l);
-            mbar_wait(&SB.bar, bkphase);
-            bkphase ^= 1u;
 #pragma unroll
-            for (int k = 0; k < P; k++) {
-                const int q = msub + L * k;
-                if (q < 8) {
-                    double2 o = make_double2(0.0, 0.0);
+        for (int k = 0; k < P; k++) {
+            const int q = msub + L * k;
+            if (q < 8) {
+                double2 o = make_double2(0.0, 0.0);
 #pragma unroll
-                    for (int r = 0; r < ROWS; r++)
-                        mac(o, S.F[r][q * 64 + t], SB.bk[r][mcomp][q * 64 + t]);
-                    S.O[mcomp][q * 64 + t] = o;
-                }
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < P; k++) {
-                const int q = msub + L * k;
-                if (q < 8) {
-                    double2 o = make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int r = 0; r < ROWS; r++)
-                        mac(o, S.F[r][q * 64 + t], bkv[r][k]);
-                    S.O[mcomp][q * 64 + t] = o;
-                }
+                for (int r = 0; r < ROWS; r++)
+                    mac(o, S.F[r][q * 64 + t], bkv[r][k]);
+                S.O[mcomp][q * 64 + t] = o;
             }
         }
         __syncthreads();
-        if constexpr (kLatTma<L>) {  // BK buffer free: stream the next step's BK
-            if (threadIdx.x == 0)
-                issue_bk(i + 1);
-        }
         // groups 0 / 1: inverse transform of output component g, ACC update
         if (g < 2) {
             const int comp = g;
@@ -1254,13 +768,12 @@ __global__ void __launch_bounds__(128 * L, 1)
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 o[q] = S.O[comp][q * 64 + t];
-#if !LAT_SKIP_INV
-            fft_inverse(o, tw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
-#endif
+            const InvTw itw = load_inv_tw(tb.inv, t);
+            fft_inverse(o, itw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
                 const int j = t + 64 * q;
-                const double2 w = cmul(o[q], untwist(S.tws[j]));
+                const double2 w = cmul(o[q], untwist(twt, q));
                 S.acc[comp][j] += (uint32_t)__double2ll_rn(w.x);
                 S.acc[comp][j + 512] += (uint32_t)__double2ll_rn(w.y);
             }

@@ -20,12 +20,26 @@ def test_fft_roundtrip_and_tables(oracle):
     assert W.shape == (256, 2) and tuple(W[0]) == (1.0, 0.0) and tuple(W[128]) == (-0.0, 1.0)
     for k in range(128):  # W[k + 128] = i * W[k] exactly
         assert W[k + 128][0] == -W[k][1] and W[k + 128][1] == W[k][0]
+    assert np.array_equal(UT[:, 0], TW[:, 0]) and np.array_equal(UT[:, 1], -TW[:, 1])
     rng = np.random.default_rng(1)
     a = rng.integers(-2 ** 31, 2 ** 31, 1024).astype(np.int32)
-    F = oracle.fft_forward(a)
+    F = oracle.fft_forward(a) / 512  # the 1/M scale lives in the BK (exact)
     acc = np.zeros(1024, np.uint32)
     oracle.fft_inverse_add(F, acc)
     assert np.array_equal(acc.view(np.int32), a)
+
+
+def test_forward_is_the_twisted_dft_in_bit_reversed_order(oracle):
+    """The absorbed-twist Cooley-Tukey forward computes Z_k = sum_j a_j psi^j W^{jk}
+    (a_j = d_j + i d_{j+512}) with Z_k in slot bitrev9(k)."""
+    rng = np.random.default_rng(3)
+    d = rng.integers(-512, 512, 1024)
+    F = oracle.fft_forward(d.astype(np.int32))
+    z = F[:, 0] + 1j * F[:, 1]
+    a = (d[:512] + 1j * d[512:]) * np.exp(1j * np.pi * np.arange(512) / 1024)
+    Z = np.fft.ifft(a) * 512
+    brv = [int(format(b, "09b")[::-1], 2) for b in range(512)]
+    assert np.max(np.abs(z - Z[brv])) < 1e-9
 
 
 @pytest.mark.parametrize("level", [80, 128])
@@ -37,6 +51,34 @@ def test_fft_product_equals_exact_product(oracle, level, okeys80, okeys128):
         e = K.external_product(i, tr, oracle.EXACT)
         f = K.external_product(i, tr, oracle.FFT)
         assert np.array_equal(e, f)
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_fft_margin_on_adversarial_maximum_digits(oracle, level, okeys80, okeys128):
+    """the FFT rounding margin on maximum-magnitude gadget digits (every digit
+    -Bg/2 or Bg/2 - 1: constant, alternating and random-sign patterns) -- external
+    products stay equal to the exact product and the margin stays far below 1/2."""
+    K = okeys80 if level == 80 else okeys128
+    l, bgbit = (2, 10) if level == 80 else (3, 7)
+    half = 1 << (bgbit - 1)
+    off = sum(half << (32 - q * bgbit) for q in range(1, l + 1)) + (1 << (31 - l * bgbit))
+
+    def word(d):  # torus word whose l digits all equal d
+        return (sum((d + half) << (32 - q * bgbit) for q in range(1, l + 1)) - off) % 2 ** 32
+
+    lo, hi = word(-half), word(half - 1)
+    rng = np.random.default_rng(level)
+    pats = [np.full(2 * K.N, lo), np.full(2 * K.N, hi),
+            np.array([lo if j % 2 else hi for j in range(2 * K.N)])]
+    pats += [np.where(rng.integers(0, 2, 2 * K.N) == 1, lo, hi) for _ in range(6)]
+    oracle.fft_margin(True)
+    for tr in pats:
+        tr = np.asarray(tr, np.uint64).astype(np.uint32)
+        for i in (0, K.n - 1):
+            assert np.array_equal(K.external_product(i, tr, oracle.FFT),
+                                  K.external_product(i, tr, oracle.EXACT))
+    m = oracle.fft_margin(True)
+    assert 0.0 < m < (0.25 if level == 80 else 1.0 / 16), m
 
 
 def test_full_blind_rotation_fft_equals_exact(oracle, okeys80):
