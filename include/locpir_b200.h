@@ -68,7 +68,9 @@ typedef struct locpir_b200_params {
     double alpha_bk;  /* bootstrapping-key noise stddev */
 } locpir_b200_params;
 
-/* One gate of a program.  Operands index n-dim slots of the context's device pool. */
+/* One gate of a program.  Operands index n-dim slots of the context's device pool;
+ * unused operands are LOCPIR_B200_NONE_SLOT (CONST carries its bit in in0). */
+#define LOCPIR_B200_NONE_SLOT 0xFFFFFFFFu
 typedef struct locpir_b200_gate_op {
     uint32_t kind;
     uint32_t in0, in1, in2;
@@ -89,6 +91,13 @@ size_t locpir_b200_ksk_words(const locpir_b200_params* p); /* KSK words [N][t][b
  * torus.hpp:119-138).  Any output pointer may be NULL to skip it. */
 int locpir_b200_keygen(const locpir_b200_params* p, uint64_t seed, uint8_t* lwe_key,
                        uint8_t* trlwe_key, uint32_t* bk, uint32_t* ksk);
+/* The same derivation around a caller's LWE key (n bytes, 0/1), e.g. a reference
+ * SecretKey from keygen(params, key_seed) (torus.hpp:146-154): the TRLWE key, BK and KSK
+ * come from `seed` exactly as in locpir_b200_keygen, which this equals when
+ * lwe_key == keygen(n, seed). */
+int locpir_b200_keygen_with_lwe_key(const locpir_b200_params* p, uint64_t seed,
+                                    const uint8_t* lwe_key, uint8_t* trlwe_key, uint32_t* bk,
+                                    uint32_t* ksk);
 /* encrypt_bit (torus.hpp:172-175) of bits[i] with NoiseSampler(seed, alpha_in),
  * drawn in order i = 0..count-1; out is [count][n+1]. */
 int locpir_b200_encrypt_bits(const locpir_b200_params* p, const uint8_t* lwe_key, uint64_t seed,

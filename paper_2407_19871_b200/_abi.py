@@ -42,6 +42,7 @@ SIGNATURES = [
     ("locpir_b200_bk_words", C.c_size_t, [_P]),
     ("locpir_b200_ksk_words", C.c_size_t, [_P]),
     ("locpir_b200_keygen", C.c_int, [_P, C.c_uint64, _u8p, _u8p, _u32p, _u32p]),
+    ("locpir_b200_keygen_with_lwe_key", C.c_int, [_P, C.c_uint64, _u8p, _u8p, _u32p, _u32p]),
     ("locpir_b200_encrypt_bits", C.c_int, [_P, _u8p, C.c_uint64, _u8p, C.c_uint64, _u32p]),
     ("locpir_b200_decrypt_bits", C.c_int, [_P, _u8p, _u32p, C.c_uint64, _u8p]),
     ("locpir_b200_ctx_create", C.c_int, [_P, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),

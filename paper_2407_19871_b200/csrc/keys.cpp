@@ -87,14 +87,39 @@ size_t locpir_b200_ksk_words(const locpir_b200_params* p)
     return valid(p) ? (size_t)p->N * p->ks_t * ((1u << p->ks_basebit) - 1) * (p->n + 1) : 0;
 }
 
+static int keygen_impl(const locpir_b200_params* p, uint64_t seed, const uint8_t* lwe_key_in,
+                       uint8_t* lwe_key_out, uint8_t* trlwe_key_out, uint32_t* bk_out,
+                       uint32_t* ksk_out);
+
 int locpir_b200_keygen(const locpir_b200_params* p, uint64_t seed, uint8_t* lwe_key_out,
                        uint8_t* trlwe_key_out, uint32_t* bk_out, uint32_t* ksk_out)
+{
+    return keygen_impl(p, seed, nullptr, lwe_key_out, trlwe_key_out, bk_out, ksk_out);
+}
+
+int locpir_b200_keygen_with_lwe_key(const locpir_b200_params* p, uint64_t seed,
+                                    const uint8_t* lwe_key, uint8_t* trlwe_key_out,
+                                    uint32_t* bk_out, uint32_t* ksk_out)
+{
+    if (!lwe_key)
+        return LOCPIR_B200_EINVAL;
+    for (uint32_t i = 0; valid(p) && i < p->n; i++)
+        if (lwe_key[i] > 1)
+            return LOCPIR_B200_EINVAL;
+    return keygen_impl(p, seed, lwe_key, nullptr, trlwe_key_out, bk_out, ksk_out);
+}
+
+static int keygen_impl(const locpir_b200_params* p, uint64_t seed, const uint8_t* lwe_key_in,
+                       uint8_t* lwe_key_out, uint8_t* trlwe_key_out, uint32_t* bk_out,
+                       uint32_t* ksk_out)
 {
     if (!valid(p))
         return LOCPIR_B200_EINVAL;
     const uint32_t n = p->n, N = p->N, l = p->bk_l, rows = 2 * l;
     std::vector<uint8_t> s(n), z(N);
-    {
+    if (lwe_key_in) {
+        std::memcpy(s.data(), lwe_key_in, n);
+    } else {
         std::mt19937_64 rng(seed);  // torus.hpp:149-152
         for (auto& b : s)
             b = static_cast<uint8_t>(rng() & 1);
