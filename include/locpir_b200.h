@@ -257,6 +257,14 @@ typedef struct locpir_b200_server locpir_b200_server;
 int locpir_b200_server_create(locpir_b200_ctx* c, const int64_t* boxes, const uint64_t* services,
                               uint32_t R, uint32_t l, uint32_t m, uint32_t max_sessions,
                               int folded, locpir_b200_server** out);
+/* The server owns every pool slot from base_slot on (server_create: base_slot = 0, i.e. a
+ * dedicated context).  While it exists, any other call on the context that reads or
+ * writes one of those slots fails with EINVAL -- e.g. a GateEngine sharing the context
+ * must keep its slots below base_slot.  One server per context; destroy the server
+ * before its context. */
+int locpir_b200_server_create_at(locpir_b200_ctx* c, uint64_t base_slot, const int64_t* boxes,
+                                 const uint64_t* services, uint32_t R, uint32_t l, uint32_t m,
+                                 uint32_t max_sessions, int folded, locpir_b200_server** out);
 void locpir_b200_server_destroy(locpir_b200_server* s);
 const char* locpir_b200_server_last_error(const locpir_b200_server* s);
 int locpir_b200_server_open_session(locpir_b200_server* s, const uint8_t* zero_sheet, uint64_t len,

@@ -97,6 +97,9 @@ SIGNATURES = [
     ("locpir_b200_server_create", C.c_int,
      [_ctx, C.POINTER(C.c_int64), _u64p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
       C.POINTER(C.c_void_p)]),
+    ("locpir_b200_server_create_at", C.c_int,
+     [_ctx, C.c_uint64, C.POINTER(C.c_int64), _u64p, C.c_uint32, C.c_uint32, C.c_uint32,
+      C.c_uint32, C.c_int, C.POINTER(C.c_void_p)]),
     ("locpir_b200_server_destroy", None, [C.c_void_p]),
     ("locpir_b200_server_last_error", C.c_char_p, [C.c_void_p]),
     ("locpir_b200_server_open_session", C.c_int,

@@ -8,7 +8,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -119,6 +121,15 @@ struct locpir_b200_ctx {
     int small_levels = 1;
     int use_graphs = 1;   // LOCPIR_B200_GRAPH=0: programs launch without CUDA graphs
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
+    // persisting-L2 window over the frequency-domain BK, attached per K1 launch (never to
+    // the caller's stream); the device-wide persisting limit is released by the last
+    // context that set it
+    bool have_window = false;
+    cudaAccessPolicyWindow bk_window{};
+    // A batching server on this context owns every pool slot >= server_base; calls from
+    // anything else that touch those slots fail (EINVAL) instead of corrupting it.
+    uint64_t server_base = UINT64_MAX;
+    int server_calls = 0;  // > 0 while a locpir_b200_server_* entry point runs
     DevBuf<uint32_t> ks_partial;
     DevBuf<uint32_t> h2d_stage;  // packed rows for 1-D host copies (k_repack_rows)
     DevBuf<uint32_t> d2h_stage;  // packed rows for 1-D device-to-host copies (k_pack_rows)
@@ -251,16 +262,33 @@ Tables make_tables(uint32_t N)
 
 FftTabs tabs(const locpir_b200_ctx* c) { return FftTabs{c->ftw.p, c->itw.p, c->TW.p}; }
 
+// contexts per device that hold a persisting-L2 BK window
+int persist_users(int device, int delta)
+{
+    static std::mutex mu;
+    static std::map<int, int> users;
+    std::lock_guard<std::mutex> g(mu);
+    return users[device] += delta;
+}
+
 void need_keys(locpir_b200_ctx* c)
 {
     if (!c->have_keys)
         throw std::logic_error("bootstrapping and key-switching keys are not uploaded");
 }
 
+void check_owned(const locpir_b200_ctx* c, uint64_t slot_end)
+{
+    if (!c->server_calls && slot_end > c->server_base)
+        throw std::invalid_argument("pool slots from " + std::to_string(c->server_base) +
+                                    " on are owned by the batching server on this context");
+}
+
 void check_pool(locpir_b200_ctx* c, uint64_t first, uint64_t count)
 {
     if (first + count > c->pool_slots || first + count < first)
         throw std::invalid_argument("pool slot range out of bounds");
+    check_owned(c, first + count);
 }
 
 void timed_begin(locpir_b200_ctx* c, int k)
@@ -299,14 +327,30 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
                 c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
-    } else if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-        k_blind_rotate<3, 7><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
-                                                         c->bkf.p, tb, mu);
-    else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-        k_blind_rotate<2, 10><<<count, 64, 0, c->stream>>>(c->dp, items, c->pool_n.p, c->pool_N.p,
-                                                          c->bkf.p, tb, mu);
-    else
-        throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(count);
+        cfg.blockDim = dim3(64);
+        cfg.stream = c->stream;
+        cudaLaunchAttribute attr[1];
+        if (c->have_window) {  // keep BK_freq L2-resident for this launch
+            attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+            attr[0].val.accessPolicyWindow = c->bk_window;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+        }
+        const uint32_t* pn = c->pool_n.p;
+        uint32_t* pN = c->pool_N.p;
+        const double2* bk = c->bkf.p;
+        if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
+            CK(cudaLaunchKernelEx(&cfg, k_blind_rotate<3, 7>, c->dp, items, pn, pN, bk, tb, mu,
+                                  (unsigned long long*)nullptr));
+        else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
+            CK(cudaLaunchKernelEx(&cfg, k_blind_rotate<2, 10>, c->dp, items, pn, pN, bk, tb, mu,
+                                  (unsigned long long*)nullptr));
+        else
+            throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
+    }
     CK(cudaGetLastError());
     timed_end(c, 0);
 }
@@ -357,6 +401,9 @@ void validate_slots(locpir_b200_ctx* c, const locpir_b200_gate_op* ops, uint64_t
                                             " outside the pool");
         if (op.out >= c->pool_slots)
             throw std::invalid_argument("output slot outside the pool");
+        for (uint32_t s : {op.in0, op.in1, op.in2, op.out})
+            if (s != SLOT_NONE && !(op.kind == LOCPIR_B200_CONST && s == op.in0 && s != op.out))
+                check_owned(c, (uint64_t)s + 1);
     }
 }
 
@@ -603,6 +650,12 @@ void locpir_b200_ctx_destroy(locpir_b200_ctx* c)
     cudaSetDevice(c->device);
     if (c->stream)
         cudaStreamSynchronize(c->stream);
+    if (c->have_window && persist_users(c->device, -1) == 0) {
+        // the last context with a BK window: hand the persisting L2 back
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        cudaGetLastError();
+    }
     for (auto& v : c->timer.ev)
         for (auto e : v)
             cudaEventDestroy(e);
@@ -645,23 +698,24 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
                              c->stream));
         CK(cudaStreamSynchronize(c->stream));
         c->have_keys = true;
-        // Keep the frequency-domain BK resident in L2 (persisting access window): at cfg2
-        // scale the blind-rotate CTAs sweep all 62 MB of it out of step with each other.
+        // Keep the frequency-domain BK resident in L2 (persisting access window, attached
+        // to every K1 launch): at cfg2 scale the blind-rotate CTAs sweep all 62 MB of it out
+        // of step with each other.
         if (c->l2_persist) {
             int maxp = 0, maxw = 0;
             cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
             cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
             const size_t bytes = c->bkf.n * sizeof(double2);
             if (maxp > 0 && maxw > 0) {
-                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, maxp));
-                cudaStreamAttrValue v{};
-                v.accessPolicyWindow.base_ptr = c->bkf.p;
-                v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, maxw);
-                v.accessPolicyWindow.hitRatio =
-                    std::min(1.0f, (float)std::min<size_t>(bytes, maxp) / (float)v.accessPolicyWindow.num_bytes);
-                v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-                v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-                cudaStreamSetAttribute(c->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+                if (!c->have_window && persist_users(c->device, +1) == 1)
+                    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp);
+                cudaAccessPolicyWindow& w = c->bk_window;
+                w.base_ptr = c->bkf.p;
+                w.num_bytes = std::min<size_t>(bytes, maxw);
+                w.hitRatio = std::min(1.0f, (float)std::min<size_t>(bytes, maxp) / (float)w.num_bytes);
+                w.hitProp = cudaAccessPropertyPersisting;
+                w.missProp = cudaAccessPropertyStreaming;
+                c->have_window = true;
                 cudaGetLastError();
             }
         }
@@ -1201,16 +1255,41 @@ int locpir_b200_pool_store_responses(locpir_b200_ctx* c, const uint32_t* out_fir
 }
 
 // ---- cross-session batcher (server.hpp) ---------------------------------------------
+// locpir_b200_server_* entry points may touch the slots the server owns
+struct ServerScope {
+    locpir_b200_ctx* c;
+    explicit ServerScope(locpir_b200_server* s) : c(s ? s->ctx : nullptr)
+    {
+        if (c)
+            c->server_calls++;
+    }
+    ~ServerScope()
+    {
+        if (c)
+            c->server_calls--;
+    }
+};
+
 int locpir_b200_server_create(locpir_b200_ctx* c, const int64_t* boxes, const uint64_t* services,
                               uint32_t R, uint32_t l, uint32_t m, uint32_t max_sessions,
                               int folded, locpir_b200_server** out)
 {
+    return locpir_b200_server_create_at(c, 0, boxes, services, R, l, m, max_sessions, folded, out);
+}
+
+int locpir_b200_server_create_at(locpir_b200_ctx* c, uint64_t base_slot, const int64_t* boxes,
+                                 const uint64_t* services, uint32_t R, uint32_t l, uint32_t m,
+                                 uint32_t max_sessions, int folded, locpir_b200_server** out)
+{
     if (!c || !boxes || !services || !out || !R || l < 2 || l > 63 || !m || m >= 64 ||
-        !max_sessions)
+        !max_sessions || base_slot >= 0xFFFFFFF0ull)
         return LOCPIR_B200_EINVAL;
     *out = nullptr;
+    if (c->server_base != UINT64_MAX)
+        return fail(c, LOCPIR_B200_ELOGIC, "a batching server already owns this context's pool tail");
     auto s = std::make_unique<locpir_b200_server>();
     s->ctx = c;
+    s->base = (uint32_t)base_slot;
     s->R = R;
     s->l = l;
     s->m = m;
@@ -1219,6 +1298,8 @@ int locpir_b200_server_create(locpir_b200_ctx* c, const int64_t* boxes, const ui
     s->folded = folded ? 1 : 0;
     s->boxes.assign(boxes, boxes + (size_t)R * 4);
     s->services.assign(services, services + R);
+    c->server_base = base_slot;  // claimed now; released below if creation fails
+    ServerScope scope(s.get());
     const int rc = lpb::srv_guard(s.get(), [&] {
         for (int64_t v : s->boxes)
             if (v < -(1ll << (l - 1)) || v >= (1ll << (l - 1)))
@@ -1231,13 +1312,19 @@ int locpir_b200_server_create(locpir_b200_ctx* c, const int64_t* boxes, const ui
     });
     if (rc) {
         c->err = s->err;
+        c->server_base = UINT64_MAX;
         return rc;
     }
     *out = s.release();
     return LOCPIR_B200_OK;
 }
 
-void locpir_b200_server_destroy(locpir_b200_server* s) { delete s; }
+void locpir_b200_server_destroy(locpir_b200_server* s)
+{
+    if (s && s->ctx)
+        s->ctx->server_base = UINT64_MAX;  // the pool tail is free again
+    delete s;
+}
 
 const char* locpir_b200_server_last_error(const locpir_b200_server* s)
 {
@@ -1247,6 +1334,7 @@ const char* locpir_b200_server_last_error(const locpir_b200_server* s)
 int locpir_b200_server_open_session(locpir_b200_server* s, const uint8_t* zero_sheet, uint64_t len,
                                     uint32_t* session)
 {
+    ServerScope scope(s);
     return lpb::srv_guard(s, [&] {
         if (!session || (len && !zero_sheet))
             throw std::invalid_argument("open_session: bad arguments");
@@ -1256,6 +1344,7 @@ int locpir_b200_server_open_session(locpir_b200_server* s, const uint8_t* zero_s
 
 int locpir_b200_server_close_session(locpir_b200_server* s, uint32_t session)
 {
+    ServerScope scope(s);
     return lpb::srv_guard(s, [&] {
         if (session >= s->max_sessions || !s->open[session])
             throw std::invalid_argument("unknown session");
@@ -1269,6 +1358,7 @@ int locpir_b200_server_close_session(locpir_b200_server* s, uint32_t session)
 int locpir_b200_server_submit(locpir_b200_server* s, uint32_t session, const uint8_t* query,
                               uint64_t len, uint64_t* ticket)
 {
+    ServerScope scope(s);
     return lpb::srv_guard(s, [&] {
         if (!ticket || (len && !query))
             throw std::invalid_argument("submit: bad arguments");
@@ -1280,6 +1370,7 @@ uint64_t locpir_b200_server_pending(const locpir_b200_server* s) { return s ? s-
 
 int locpir_b200_server_flush(locpir_b200_server* s, uint64_t* answered)
 {
+    ServerScope scope(s);
     return lpb::srv_guard(s, [&] {
         const uint64_t n = lpb::srv_flush(s);
         if (answered)

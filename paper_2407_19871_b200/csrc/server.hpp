@@ -26,6 +26,7 @@ struct locpir_b200_server {
     int folded = 0;
     std::vector<int64_t> boxes;      // [R][4] signed grid values
     std::vector<uint64_t> services;  // [R] service values (the server's dataset)
+    uint32_t base = 0;  // first pool slot the server owns (locpir_b200_server_create_at)
     uint32_t bnd_first = 0, svc_area = 0, flush_first = 0;
     std::vector<uint8_t> open;       // per session slot block
     struct Pending {
@@ -63,9 +64,10 @@ inline uint32_t grid_bit(int64_t v, uint32_t i) { return (uint32_t)(((uint64_t)v
 
 inline void srv_init(locpir_b200_server* s)
 {
-    // pool: [R*4*l trivial boundary words][max_sessions * R*m service slots][flush area]
-    s->bnd_first = 0;
-    s->svc_area = s->folded ? 0 : s->R * 4 * s->l;
+    // pool from `base`: [R*4*l trivial boundary words][max_sessions * R*m service slots]
+    // [flush area]
+    s->bnd_first = s->base;
+    s->svc_area = s->base + (s->folded ? 0 : s->R * 4 * s->l);
     s->flush_first = s->svc_area + s->max_sessions * s->R * s->m;
     srv_ck(s, locpir_b200_pool_reserve(s->ctx, s->flush_first));
     if (!s->folded) {  // dataset.hpp:250-253: boundaries as trivial words

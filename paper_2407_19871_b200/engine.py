@@ -475,6 +475,7 @@ class CipherBit:
     """One encrypted bit living in a device pool slot (gate_engine.hpp:81-109)."""
     engine_id: int
     slot: int
+    epoch: int = 0  # slot-arena generation (GateEngine.reset_slots)
 
     def kind(self) -> str:
         return "tfhe-b200"
@@ -491,6 +492,8 @@ class GateEngine:
         self._seed = seed
         self._enc_counter = 0
         self._next_slot = 0
+        self._epoch = 0
+        self._limit = 0xFFFFFFF0  # first slot this engine may not use
         self._pending: list | None = None
         self._fork_blocks = [0]
 
@@ -506,7 +509,10 @@ class GateEngine:
         return "tfhe-b200"
 
     def fork(self, lane: int) -> "GateEngine":
-        return self  # deterministic bootstrap: nothing to fork
+        # deterministic bootstrap: nothing to fork.  The mirror is not
+        # thread-safe (one host thread per engine, like a reference GateEngine,
+        # gate_engine.hpp:335); the C++ integration header supports concurrent forks.
+        return self
 
     def acquire_fork_block(self) -> int:
         b = self._fork_blocks[0]
@@ -523,17 +529,39 @@ class GateEngine:
     def counters_reset(self):
         self.ctx.counters_reset()
 
+    def reset_slots(self):
+        """Slot arena: every gate output owns one pool slot until this call; a long-running
+        caller resets between independent evaluations.  Older bits are then rejected."""
+        self.flush()
+        self._next_slot = 0
+        self._epoch += 1
+
+    def slots_in_use(self) -> int:
+        return self._next_slot
+
+    def reserve_server_tail(self, headroom: int = 1 << 16) -> int:
+        """Cap this engine below the returned slot and hand the pool tail to a
+        BatchingServer on the same context (BatchingServer(..., base_slot=...))."""
+        self.flush()
+        self._limit = min(self._limit, self._next_slot + headroom)
+        return self._limit
+
     def _alloc(self, k: int = 1) -> int:
         s = self._next_slot
+        if s + k > self._limit:
+            raise LogicError(f"engine slot range exhausted at slot {s} (reset_slots() between "
+                             "evaluations, or a server owns the pool tail)")
         self._next_slot += k
         if self._next_slot > self.ctx.pool_capacity:
             self.flush()
-            self.ctx.pool_reserve(max(self._next_slot, 2 * self.ctx.pool_capacity))
+            self.ctx.pool_reserve(min(self._limit, max(self._next_slot, 2 * self.ctx.pool_capacity)))
         return s
 
     def _bit(self, c: CipherBit) -> int:
         if not isinstance(c, CipherBit) or c.engine_id != self._id:
             raise InvalidArgument("cipher bit belongs to a different engine")
+        if c.epoch != self._epoch:
+            raise InvalidArgument("cipher bit predates reset_slots()")
         return c.slot
 
     def _emit(self, kind, a=_abi.SLOT_NONE, b=_abi.SLOT_NONE, c=_abi.SLOT_NONE) -> CipherBit:
@@ -543,7 +571,7 @@ class GateEngine:
             self._pending.append(op)
         else:
             self.ctx.run([op])
-        return CipherBit(self._id, out)
+        return CipherBit(self._id, out, self._epoch)
 
     @contextlib.contextmanager
     def batch(self):
@@ -582,7 +610,7 @@ class GateEngine:
         self.flush()
         first = self._alloc(cts.shape[0])
         self.ctx.h2d(first, cts)
-        return [CipherBit(self._id, first + i) for i in range(cts.shape[0])]
+        return [CipherBit(self._id, first + i, self._epoch) for i in range(cts.shape[0])]
 
     def sample(self, c: CipherBit) -> np.ndarray:
         self.flush()

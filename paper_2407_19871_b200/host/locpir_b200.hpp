@@ -12,9 +12,12 @@
 // follow circuits.hpp:187-324 gate for gate.
 #pragma once
 
+#include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -108,8 +111,9 @@ public:
 
 private:
     friend class GateEngine;
-    CipherBit(uint64_t engine, uint32_t slot) : engine_(engine), slot_(slot) {}
+    CipherBit(uint64_t engine, uint64_t epoch, uint32_t slot) : engine_(engine), epoch_(epoch), slot_(slot) {}
     uint64_t engine_ = 0;
+    uint64_t epoch_ = 0;  // slot arena generation (GateEngine::reset_slots)
     uint32_t slot_ = 0xFFFFFFFFu;
 };
 
@@ -139,9 +143,11 @@ public:
     }
 
     EngineKind kind() const { return EngineKind::TfheB200; }
-    // Deterministic bootstrap: forks share state; kept for the API.
+    // Deterministic bootstrap: forks share the recorder (one context, every mutating call
+    // under the State mutex), so gates on distinct bits may be recorded from concurrent
+    // forks as the reference's circuits do (gate_engine.hpp:128-129).
     GateEngine fork(uint64_t /*lane*/) const { return *this; }
-    uint64_t acquire_fork_block() const { return st_->fork_blocks++; }
+    uint64_t acquire_fork_block() const { return st_->fork_blocks.fetch_add(1); }
     const Params& params() const { return st_->keys.params; }
     const std::vector<uint8_t>& secret_key() const { return st_->keys.lwe_key; }
 
@@ -161,17 +167,19 @@ public:
     CipherBit encrypt(bool b) { return encrypt_many({static_cast<uint8_t>(b)})[0]; }
     std::vector<CipherBit> encrypt_many(const std::vector<uint8_t>& bits)
     {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
         flush();
         const auto cts = st_->keys.encrypt(bits, st_->seed + st_->enc_calls++);
-        const uint32_t first = alloc((uint32_t)bits.size());
+        const uint32_t first = alloc(bits.size());
         check(locpir_b200_pool_h2d(st_->ctx, first, bits.size(), cts.data()), st_->ctx);
         std::vector<CipherBit> out;
         for (uint32_t i = 0; i < bits.size(); i++)
-            out.push_back(CipherBit(st_->id, first + i));
+            out.push_back(CipherBit(st_->id, st_->epoch, first + i));
         return out;
     }
     std::vector<uint32_t> sample(const CipherBit& c)
     {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
         flush();
         std::vector<uint32_t> out(params().sample_words());
         check(locpir_b200_pool_d2h(st_->ctx, slot(c), 1, out.data()), st_->ctx);
@@ -204,15 +212,44 @@ public:
         return st_->ctx;
     }
 
+    // Slot arena.  Every gate output owns one pool slot (n+1 words) until reset_slots():
+    // a long-running caller (e.g. one loc_pir per query) resets between independent
+    // evaluations.  Bits from before a reset are rejected (invalid_argument), never aliased.
+    void reset_slots()
+    {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
+        flush();
+        st_->next_slot = 0;
+        st_->epoch++;
+    }
+    uint64_t slots_in_use() const { return st_->next_slot; }
+
+    // Caps this engine's slots below the returned base and hands [base, ...) to a
+    // BatchingServer on the same context (locpir_b200_server_create_at).  `headroom`
+    // more slots stay available to the engine.
+    uint64_t reserve_server_tail(uint64_t headroom = 1u << 16)
+    {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
+        flush();
+        st_->limit = std::min<uint64_t>(st_->limit, st_->next_slot + headroom);
+        return st_->limit;
+    }
+
     // -- level batching ---------------------------------------------------------
-    void begin_batch() { st_->batching++; }
+    void begin_batch()
+    {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
+        st_->batching++;
+    }
     void end_batch()
     {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
         if (st_->batching > 0 && --st_->batching == 0)
             flush();
     }
     void flush()
     {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
         if (st_->pending.empty())
             return;
         std::vector<locpir_b200_gate_op> ops;
@@ -225,10 +262,12 @@ private:
         ClientKeys keys;
         locpir_b200_ctx* ctx = nullptr;
         uint64_t id = 0, seed = 0, enc_calls = 0;
-        uint32_t next_slot = 0;
+        uint64_t next_slot = 0, epoch = 0;
+        uint64_t limit = 0xFFFFFFF0ull;  // first slot the engine may not use
         uint64_t capacity = 0;
         int batching = 0;
-        mutable uint64_t fork_blocks = 0;
+        std::atomic<uint64_t> fork_blocks{0};
+        std::recursive_mutex mu;
         std::vector<locpir_b200_gate_op> pending;
         explicit State(const ClientKeys& k) : keys(k) {}
         ~State()
@@ -256,20 +295,26 @@ private:
         check(locpir_b200_pool_reserve(st_->ctx, want), st_->ctx);
         st_->capacity = locpir_b200_pool_capacity(st_->ctx);
     }
-    uint32_t alloc(uint32_t k)
+    uint32_t alloc(uint64_t k)
     {
-        const uint32_t s = st_->next_slot;
+        const uint64_t s = st_->next_slot;
+        if (s + k > st_->limit)
+            throw std::logic_error("engine slot range exhausted at slot " + std::to_string(s) +
+                                   " (reset_slots() between evaluations, or a server owns the "
+                                   "pool tail)");
         st_->next_slot += k;
         if (st_->next_slot > st_->capacity) {
             flush();
-            grow(std::max<uint64_t>(st_->next_slot, 2 * st_->capacity));
+            grow(std::min<uint64_t>(st_->limit, std::max<uint64_t>(st_->next_slot, 2 * st_->capacity)));
         }
-        return s;
+        return static_cast<uint32_t>(s);
     }
     uint32_t slot(const CipherBit& c) const
     {
         if (c.engine_ != st_->id)
             throw std::invalid_argument("cipher bit belongs to a different engine");
+        if (c.epoch_ != st_->epoch)
+            throw std::invalid_argument("cipher bit predates reset_slots()");
         return c.slot_;
     }
     CipherBit emit2(uint32_t kind, const CipherBit& a, const CipherBit& b)
@@ -278,11 +323,12 @@ private:
     }
     CipherBit emit(uint32_t kind, uint32_t a, uint32_t b = 0xFFFFFFFFu, uint32_t c = 0xFFFFFFFFu)
     {
+        std::lock_guard<std::recursive_mutex> g(st_->mu);
         const uint32_t out = alloc(1);
         st_->pending.push_back({kind, a, b, c, out});
         if (!st_->batching)
             flush();
-        return CipherBit(st_->id, out);
+        return CipherBit(st_->id, st_->epoch, out);
     }
 
     std::shared_ptr<State> st_;
@@ -436,9 +482,12 @@ public:
     {
         if (boxes.size() != services.size() * 4)
             throw std::invalid_argument("one service value per box");
+        // the server owns the pool tail from the engine's cap on (no shared slots)
+        const uint64_t base = eng.reserve_server_tail();
         locpir_b200_ctx* c = eng.native();
-        check(locpir_b200_server_create(c, boxes.data(), services.data(), (uint32_t)services.size(),
-                                        l, m, max_sessions, folded ? 1 : 0, &s_),
+        check(locpir_b200_server_create_at(c, base, boxes.data(), services.data(),
+                                           (uint32_t)services.size(), l, m, max_sessions,
+                                           folded ? 1 : 0, &s_),
               c);
     }
     ~BatchingServer() { locpir_b200_server_destroy(s_); }

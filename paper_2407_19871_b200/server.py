@@ -15,18 +15,21 @@ from .engine import InvalidArgument, LogicError
 
 class BatchingServer:
     def __init__(self, ctx, boxes, services, l: int, m: int, max_sessions: int = 64,
-                 folded: bool = False):
-        """boxes: [R, 4] signed l-bit grid values (x1, x2, y1, y2); services: [R] values."""
+                 folded: bool = False, base_slot: int = 0):
+        """boxes: [R, 4] signed l-bit grid values (x1, x2, y1, y2); services: [R] values.
+        The server owns every pool slot from base_slot on (0: a dedicated context); other
+        calls on the context that touch those slots fail (include/locpir_b200.h)."""
         self.ctx, self.l, self.m = ctx, l, m
         bx = np.ascontiguousarray(boxes, np.int64).reshape(-1, 4)
         sv = np.ascontiguousarray(services, np.uint64).reshape(-1)
         if sv.size != bx.shape[0]:
             raise InvalidArgument("one service value per box")
         h = C.c_void_p()
-        rc = lib().locpir_b200_server_create(ctx.h, bx.ctypes.data_as(C.POINTER(C.c_int64)),
-                                             sv.ctypes.data_as(C.POINTER(C.c_uint64)),
-                                             bx.shape[0], l, m, max_sessions, int(folded),
-                                             C.byref(h))
+        rc = lib().locpir_b200_server_create_at(ctx.h, base_slot,
+                                                bx.ctypes.data_as(C.POINTER(C.c_int64)),
+                                                sv.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                bx.shape[0], l, m, max_sessions, int(folded),
+                                                C.byref(h))
         if rc:
             raise InvalidArgument(lib().locpir_b200_last_error(ctx.h).decode())
         self.h = h

@@ -193,6 +193,10 @@ int main()
         const uint32_t l = 16, m = 4;
         const std::vector<int64_t> boxes = {0, 100, 0, 100, -50, 20, -30, 10, 200, 300, -5, 5};
         const std::vector<uint64_t> services = {9, 6, 13};
+        // engine values from before the server exists must survive it (the
+        // server owns a disjoint pool tail, the engine's slots stay below it)
+        const CipherBit before1 = eng.hom_xor(eng.encrypt(1), eng.encrypt(0));
+        const CipherBit before0 = eng.hom_and(eng.encrypt(1), eng.encrypt(0));
         BatchingServer srv(eng, boxes, services, l, m, 2);
         const size_t S = keys.params.sample_words();
         auto sheet = [&](uint64_t seed) {  // Enc(-1/8) + 1/8 = Enc(0) per sample
@@ -235,6 +239,25 @@ int main()
             CHECK(v == qs[i].second);
         }
         CHECK_THROWS_AS(srv.submit(7, query(1, 1, 9)), std::logic_error);
+        // the engine keeps working next to the server, and its old values are intact
+        CHECK(eng.decrypt(before1) == 1 && eng.decrypt(before0) == 0);
+        CHECK(eng.decrypt(eng.hom_or(before1, before0)) == 1);
+        // a raw ABI call into the server's slots is refused instead of corrupting them
+        {
+            const uint64_t tail = eng.reserve_server_tail();
+            std::vector<uint32_t> row(keys.params.sample_words(), 0);
+            CHECK(locpir_b200_pool_h2d(eng.native(), tail, 1, row.data()) == LOCPIR_B200_EINVAL);
+        }
+    }
+
+    // slot arena: reset_slots() recycles the pool; bits from before a reset are rejected
+    {
+        const CipherBit old = eng.encrypt(1);
+        const uint64_t used = eng.slots_in_use();
+        eng.reset_slots();
+        CHECK(eng.slots_in_use() == 0 && used > 0);
+        CHECK_THROWS_AS(eng.decrypt(old), std::invalid_argument);
+        CHECK(eng.decrypt(eng.hom_nand(eng.encrypt(1), eng.encrypt(1))) == 0);
     }
 
     std::printf("%d checks, %d failed\n", g_checks, g_fail);

@@ -61,3 +61,41 @@ def test_sessions_batched_city_table(golden, level, folded):
         srv.submit(sessions[1], query_payload(key, smp, 1, 2, l)[0])
     srv.close()
     ctx.close()
+
+
+def test_server_and_engine_share_a_context(golden):
+    """a GateEngine and a BatchingServer on one context no longer share slots.
+    The engine caps itself below reserve_server_tail(); the server owns the tail; engine
+    values made before the server survive a flush; a raw call into the tail is refused."""
+    from test_wire import query_payload, zero_sheet_payload
+    from paper_2407_19871_b200 import ClientKeys, Context, TfheParams
+    from paper_2407_19871_b200.engine import GateEngine, InvalidArgument
+    from paper_2407_19871_b200.server import BatchingServer
+    p = TfheParams(128)
+    keys = ClientKeys(p, 41)
+    ctx = Context(p, 0)
+    ctx.upload_keys(keys.bk, keys.ksk)
+    eng = GateEngine(ctx, keys, seed=5)
+    one = eng.hom_xor(eng.encrypt(1), eng.encrypt(0))
+    zero = eng.hom_and(eng.encrypt(1), eng.encrypt(0))
+    base = eng.reserve_server_tail(headroom=64)
+    key = O.keygen_bits(p.n, 41)
+    l, m = 16, golden["city_service_bits"][0]
+    boxes = np.array(golden["city_boxes_grid_x1_x2_y1_y2_int32"], np.uint32).view(np.int32).reshape(-1, 4)
+    srv = BatchingServer(ctx, boxes, golden["city_services"], l, m, max_sessions=1, base_slot=base)
+    sheet, _ = zero_sheet_payload(key, O.NoiseSampler(300, 2.0 ** -15), boxes.shape[0], m)
+    sid = srv.open_session(sheet)
+    qs = np.array(golden["city_queries_grid_xy_int32"], np.uint32).view(np.int32).reshape(-1, 2)
+    t = srv.submit(sid, query_payload(key, O.NoiseSampler(400, 2.0 ** -15), qs[0][0], qs[0][1], l)[0])
+    srv.flush()
+    assert _decrypt(srv.take_response(t), key, m) == golden["city_expected"][0]
+    assert eng.decrypt(one) == 1 and eng.decrypt(zero) == 0
+    assert eng.decrypt(eng.hom_or(one, zero)) == 1
+    with pytest.raises(InvalidArgument, match="owned by the batching server"):
+        ctx.h2d(base, keys.encrypt_bits(np.ones(1, np.uint8), 1))
+    srv.close()
+    ctx.h2d(base, keys.encrypt_bits(np.ones(1, np.uint8), 1))  # free again
+    eng.reset_slots()
+    with pytest.raises(InvalidArgument, match="predates reset_slots"):
+        eng.decrypt(one)
+    ctx.close()
