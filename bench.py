@@ -496,8 +496,119 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
             }
             run.close()
     out["cfg4_server"] = run_server_sample(ctx128, keys128, ws, max_over_ranks)
-    if ctx80 is not None:
+    if ctx80 is not None:  # cfg1's latency roof (single query, 80-bit)
+        for key in ("cfg1", "cfg1_tree"):
+            if key in out:
+                out[key]["latency_roofline"] = latency_floor(ctx80, keys80, out[key]["levels"],
+                                                             out[key]["ms_per_batch"])
         ctx80.close()
+    if args.emulate_shards and ws == 1:
+        out["shard_emulation"] = run_shard_emulation(ctx128, keys128)
+    return out
+
+
+def device_ms(fn, reps=3, warm=True):
+    """Mean device time of fn() over reps launches (CUDA events on the current stream)."""
+    import torch
+    if warm:
+        fn()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def latency_floor(ctx, keys, levels, measured_ms):
+    """cfg1 is latency-bound (a 21-level circuit with <= 64 gates per level): its roof is
+    levels x the latency of ONE bootstrapped gate (blind rotation on the latency kernel
+    K1l + split key switch K2s), measured here with a one-gate program."""
+    from paper_2407_19871_b200 import _abi
+    ctx.pool_reserve(4)
+    ctx.h2d(0, keys.encrypt_bits(np.array([1, 0], np.uint8), 5))
+    prog = ctx.program([(_abi.NAND, 0, 1, _abi.SLOT_NONE, 2)])
+    t_gate = device_ms(prog.launch, reps=5)
+    prog.close()
+    floor = levels * t_gate
+    return {"bound": "latency", "levels": levels, "one_gate_ms": t_gate, "floor_ms": floor,
+            "measured_ms": measured_ms, "frac": floor / measured_ms,
+            "note": "floor = critical-path levels x one bootstrapped gate's device latency"}
+
+
+def run_shard_emulation(ctx, keys, Ns=(2, 4, 8)):
+    """--emulate-shards: the N-GPU LocPIR shards run one after another on
+    this one GPU.  cfg3 (box-sharded, strong scaling): every rank's box shard is evaluated
+    (xor_tree mode 2), the partial roots are copied into the rank-0 combine region and the
+    combine level runs; predicted N-GPU time = max shard time + combine time (the gather of
+    N x 32 ciphertexts over NVLink is ~us and not modelled).  cfg4/cfg5 (query-sharded):
+    the largest shard (Q/N queries) is timed; predicted time = that shard's time.  Results
+    are decrypted and checked against the plaintext truth."""
+    import torch
+    from paper_2407_19871_b200 import workloads as W
+    from paper_2407_19871_b200.dist import shard_range
+    out = {}
+    sec, Q, R, l, m, enc = W.CONFIGS["cfg3"]
+    b = W.make_batch(Q, R, l, m, seed=KEY_SEED + 3, encrypted_bounds=enc)
+    b.x[0] = (b.boxes[0, 0] + b.boxes[0, 1]) // 2
+    b.y[0] = (b.boxes[0, 2] + b.boxes[0, 3]) // 2
+    n1 = ctx.params.n + 1
+    rows = {}
+    for N in Ns:
+        spans = [shard_range(R, r, N) for r in range(N)]
+        t_shards, parts = [], []
+        for lo, hi in spans:
+            sub = W.sub_batch(b, 0, Q, lo, hi)
+            lay = W.PoolLayout(sub)
+            ctx.pool_reserve(lay.total)
+            W.load_batch(ctx, keys, sub, lay, 5000 + lo)
+            prog = ctx.program(W.program_ops(sub, lay, 2))
+            t_shards.append(device_ms(prog.launch, reps=1))
+            parts.append(ctx.d2h(int(lay.out.min()), Q * m))
+            prog.close()
+        part_first, out_first = 0, N * Q * m
+        comb_first = out_first + Q * m
+        ctx.pool_reserve(comb_first + Q * m * (N + 1))
+        ctx.h2d(part_first, np.concatenate(parts))
+        comb = ctx.program(W.combine_ops(N, Q, m, part_first, out_first, comb_first))
+        t_comb = device_ms(comb.launch, reps=1)
+        comb.close()
+        bits = keys.decrypt_bits(ctx.d2h(out_first, Q * m)).reshape(Q, m).astype(np.uint64)
+        got = (bits << np.arange(m, dtype=np.uint64)).sum(axis=1)
+        t = max(t_shards) + t_comb
+        rows[N] = {"boxes_per_gpu": spans[0][1] - spans[0][0], "max_shard_ms": max(t_shards),
+                   "combine_ms": t_comb, "predicted_ms": t, "predicted_queries_per_s": Q / (t / 1e3),
+                   "correct": bool(np.array_equal(got, b.truth()))}
+    out["cfg3"] = {"sharding": "boxes (strong scaling)", "per_N": rows}
+    for name in ("cfg4", "cfg5"):
+        sec, Q, R, l, m, enc = W.CONFIGS[name]
+        rows = {}
+        for N in Ns[-1:]:
+            lo, hi = shard_range(Q, 0, N)
+            b = W.make_batch(hi - lo, R, l, m, seed=KEY_SEED + 4, encrypted_bounds=enc)
+            for q in range(min(hi - lo, R)):
+                b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+                b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+            lay = W.PoolLayout(b, LOCPIR_CHUNK[name])
+            ctx.pool_reserve(lay.total)
+            W.load_batch(ctx, keys, b, lay, 5000)
+            progs = [ctx.program(W.program_ops(b, lay, True, q_lo=a, q_hi=z)) for a, z in lay.chunks()]
+            for p_ in progs:
+                p_.prepare()
+            t = device_ms(lambda: [p_.launch() for p_ in progs], reps=1, warm=False)
+            bits = keys.decrypt_bits(ctx.d2h(int(lay.out.min()), b.Q * m)).reshape(b.Q, m)
+            got = (bits.astype(np.uint64) << np.arange(m, dtype=np.uint64)).sum(axis=1)
+            for p_ in progs:
+                p_.close()
+            rows[N] = {"queries_per_gpu": hi - lo, "shard_ms": t,
+                       "predicted_queries_per_s": Q / (t / 1e3),
+                       "correct": bool(np.array_equal(got, b.truth()))}
+        out[name] = {"sharding": "queries (strong scaling of the stated batch)", "per_N": rows}
+    out["label"] = ("single-GPU emulation of the N-GPU shards (no multi-GPU box was "
+                    "available); not a measured multi-GPU number")
     return out
 
 
@@ -796,6 +907,8 @@ def main():
                          "sample: LOCPIR_SAMPLES queries per GPU (quick runs)")
     ap.add_argument("--gates", type=int, default=GATES_PER_GPU,
                     help="gates per GPU (default: the cfg2 size; smaller only for profiling)")
+    ap.add_argument("--emulate-shards", action="store_true",
+                    help="also run the N = 2/4/8 LocPIR shards one after another on this GPU")
     ap.add_argument("--dry-run", action="store_true",
                     help="multi-rank plumbing only (gloo, plaintext interpreter, no GPU)")
     args = ap.parse_args()

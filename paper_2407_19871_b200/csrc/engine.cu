@@ -121,6 +121,10 @@ struct locpir_b200_ctx {
     int small_levels = 1;
     int use_graphs = 1;   // LOCPIR_B200_GRAPH=0: programs launch without CUDA graphs
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
+    // env LOCPIR_B200_POISON=<u32>: newly grown pool and scratch memory is filled with this
+    // word instead of zeros / left undefined (self-check: results must not depend on it)
+    uint32_t poison = 0;
+    bool poison_set = false;
     // persisting-L2 window over the frequency-domain BK, attached per K1 launch (never to
     // the caller's stream); the device-wide persisting limit is released by the last
     // context that set it
@@ -136,6 +140,36 @@ struct locpir_b200_ctx {
 };
 
 namespace {
+
+// fill device words with v (pool growth: zeros, or the self-check poison)
+void fill_words(locpir_b200_ctx* c, uint32_t* p, size_t words, uint32_t v)
+{
+    if (!words)
+        return;
+    if (v == 0) {
+        CK(cudaMemsetAsync(p, 0, words * 4, c->stream));
+        return;
+    }
+    k_fill<<<c->num_sms * 4, 256, 0, c->stream>>>(p, words, v);
+    CK(cudaGetLastError());
+}
+// scratch (N-dim) growth: undefined contents, poisoned in self-check runs
+void grow_scratch(locpir_b200_ctx* c, uint64_t slots)
+{
+    const size_t old = c->pool_N.n;
+    c->pool_N.reserve((size_t)slots * c->dp.N_stride, c->stream, false);
+    if (c->poison_set && c->pool_N.n != old)
+        fill_words(c, c->pool_N.p, c->pool_N.n, c->poison);
+}
+
+// kernel parameters with the pool sizes current at this launch (LPB_CHECKS bounds)
+DevParams dparams(const locpir_b200_ctx* c)
+{
+    DevParams d = c->dp;
+    d.pool_slots = c->pool_slots;
+    d.scratch_slots = c->pool_N.n / c->dp.N_stride;
+    return d;
+}
 
 int fail(locpir_b200_ctx* c, int code, const std::string& msg)
 {
@@ -321,10 +355,10 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
     if (c->small_levels && count <= (uint32_t)c->num_sms) {
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
             k_blind_rotate_lat<3, 7><<<count, 128 * 3, kLatSmemBytes<3>, c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
+                dparams(c), items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
             k_blind_rotate_lat<2, 10><<<count, 128 * 2, kLatSmemBytes<2>, c->stream>>>(
-                c->dp, items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
+                dparams(c), items, c->pool_n.p, c->pool_N.p, c->bkf.p, tb, mu);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
     } else {
@@ -343,10 +377,10 @@ void launch_br(locpir_b200_ctx* c, const BrItem* items, uint32_t count)
         uint32_t* pN = c->pool_N.p;
         const double2* bk = c->bkf.p;
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
-            CK(cudaLaunchKernelEx(&cfg, k_blind_rotate<3, 7>, c->dp, items, pn, pN, bk, tb, mu,
+            CK(cudaLaunchKernelEx(&cfg, k_blind_rotate<3, 7>, dparams(c), items, pn, pN, bk, tb, mu,
                                   (unsigned long long*)nullptr));
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
-            CK(cudaLaunchKernelEx(&cfg, k_blind_rotate<2, 10>, c->dp, items, pn, pN, bk, tb, mu,
+            CK(cudaLaunchKernelEx(&cfg, k_blind_rotate<2, 10>, dparams(c), items, pn, pN, bk, tb, mu,
                                   (unsigned long long*)nullptr));
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
@@ -364,15 +398,15 @@ void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
     if (c->small_levels && blocks < (uint32_t)c->num_sms / 2) {
         c->ks_partial.reserve((size_t)count * KS_SPLIT * c->dp.n_stride, c->stream, false);
         k_keyswitch_split<<<dim3(count, KS_SPLIT), KS_THREADS, 0, c->stream>>>(
-            c->dp, items, c->pool_N.p, c->ksk.p, c->ks_partial.p);
-        k_ks_reduce<<<count, KS_THREADS, 0, c->stream>>>(c->dp, items, c->pool_N.p,
+            dparams(c), items, c->pool_N.p, c->ksk.p, c->ks_partial.p);
+        k_ks_reduce<<<count, KS_THREADS, 0, c->stream>>>(dparams(c), items, c->pool_N.p,
                                                           c->ks_partial.p, c->pool_n.p);
         CK(cudaGetLastError());
         timed_end(c, 1);
         return;
     }
     const size_t smem = (size_t)KS_CT * c->p.N * sizeof(uint16_t);
-    k_keyswitch<<<blocks, KS_THREADS, smem, c->stream>>>(c->dp, items, count, c->pool_N.p,
+    k_keyswitch<<<blocks, KS_THREADS, smem, c->stream>>>(dparams(c), items, count, c->pool_N.p,
                                                          c->pool_n.p, c->ksk.p);
     CK(cudaGetLastError());
     timed_end(c, 1);
@@ -385,7 +419,7 @@ void launch_lin(locpir_b200_ctx* c, const LinItem* items, uint32_t count)
     timed_begin(c, 2);
     const uint64_t total = (uint64_t)count * (c->p.n + 1);
     const uint32_t blocks = (uint32_t)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
-    k_linear<<<blocks, 256, 0, c->stream>>>(c->dp, items, count, c->pool_n.p);
+    k_linear<<<blocks, 256, 0, c->stream>>>(dparams(c), items, count, c->pool_n.p);
     CK(cudaGetLastError());
     timed_end(c, 2);
 }
@@ -480,7 +514,7 @@ void program_prepare(locpir_b200_ctx* c, const locpir_b200_program* pr)
     if (P.n_br)
         need_keys(c);
     if (P.scratch > c->scratch_slots) {
-        c->pool_N.reserve((size_t)P.scratch * c->dp.N_stride, c->stream, false);
+        grow_scratch(c, P.scratch);
         c->scratch_slots = c->pool_N.n / c->dp.N_stride;
     }
 }
@@ -538,7 +572,7 @@ void pool_copy(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_
         // one 1-D copy into a packed staging buffer + an HBM-speed repack kernel
         c->h2d_stage.reserve((size_t)count * (c->p.n + 1), c->stream, false);
         CK(cudaMemcpyAsync(c->h2d_stage.p, src, (size_t)count * wb, kind, c->stream));
-        k_repack_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(c->dp, c->h2d_stage.p, count,
+        k_repack_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(dparams(c), c->h2d_stage.p, count,
                                                              c->pool_n.p + first * c->dp.n_stride);
         CK(cudaGetLastError());
     } else if (to_pool) {
@@ -546,7 +580,7 @@ void pool_copy(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_
                              c->stream));
     } else if (kind == cudaMemcpyDeviceToHost && count >= 256) {
         c->d2h_stage.reserve((size_t)count * (c->p.n + 1), c->stream, false);
-        k_pack_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(c->dp, c->pool_n.p + first * c->dp.n_stride,
+        k_pack_rows<<<c->num_sms * 8, 256, 0, c->stream>>>(dparams(c), c->pool_n.p + first * c->dp.n_stride,
                                                            count, c->d2h_stage.p);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(dst, c->d2h_stage.p, (size_t)count * wb, kind, c->stream));
@@ -600,7 +634,7 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
     c->p = *p;
     c->device = device;
     const uint32_t ns = (p->n + 1 + 3) & ~3u;
-    c->dp = {p->n, p->N, p->bk_l, p->bk_bgbit, p->ks_t, p->ks_basebit, ns, p->N + 4};
+    c->dp = {p->n, p->N, p->bk_l, p->bk_bgbit, p->ks_t, p->ks_basebit, ns, p->N + 4, 0, 0};
     int rc = guarded(c.get(), [&] {
         CK(cudaSetDevice(device));
         CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -632,6 +666,11 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             c->small_levels = strcmp(sl, "0") != 0;
         if (const char* gr = getenv("LOCPIR_B200_GRAPH"))
             c->use_graphs = strcmp(gr, "0") != 0;
+        if (const char* po = getenv("LOCPIR_B200_POISON"); po && *po) {
+            c->poison = (uint32_t)strtoul(po, nullptr, 0);
+            c->poison_set = true;
+            CK(cudaMemcpyToSymbol(c_poison, &c->poison, sizeof(uint32_t)));
+        }
     });
     if (rc != LOCPIR_B200_OK) {
         fprintf(stderr, "locpir_b200_ctx_create: %s\n", c->err.c_str());
@@ -731,8 +770,8 @@ int locpir_b200_pool_reserve(locpir_b200_ctx* c, uint64_t slots)
         c->pool_n.reserve((size_t)slots * c->dp.n_stride, c->stream, true);
         const uint64_t old = c->pool_slots;
         c->pool_slots = c->pool_n.n / c->dp.n_stride;
-        CK(cudaMemsetAsync(c->pool_n.p + old * c->dp.n_stride, 0,
-                           (c->pool_slots - old) * c->dp.n_stride * 4, c->stream));
+        fill_words(c, c->pool_n.p + old * c->dp.n_stride, (c->pool_slots - old) * c->dp.n_stride,
+                   c->poison);
     });
 }
 
@@ -965,7 +1004,7 @@ int locpir_b200_debug_blind_rotate(locpir_b200_ctx* c, const uint32_t* lwe_n, ui
         for (uint64_t g = 0; g < count; g++)
             items[g] = {(uint32_t)g, SLOT_NONE, 1, 0, 0u, (uint32_t)g, SLOT_NONE, 0};
         if (count > c->scratch_slots) {
-            c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
+            grow_scratch(c, count);
             c->scratch_slots = c->pool_N.n / c->dp.N_stride;
         }
         DevBuf<BrItem> d;
@@ -993,7 +1032,7 @@ int locpir_b200_debug_keyswitch(locpir_b200_ctx* c, const uint32_t* lwe_N, uint6
                 throw CudaError(c->err);
         }
         if (count > c->scratch_slots) {
-            c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
+            grow_scratch(c, count);
             c->scratch_slots = c->pool_N.n / c->dp.N_stride;
         }
         CK(cudaMemcpy2DAsync(c->pool_N.p, (size_t)c->dp.N_stride * 4, lwe_N, (size_t)(c->p.N + 1) * 4,
@@ -1189,7 +1228,7 @@ int locpir_b200_pool_load_queries(locpir_b200_ctx* c, const uint8_t* payloads,
         CK(cudaMemcpyAsync(d_off.p, offs.data(), (count + 1) * 8, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(d_slots.p, slots.data(), 2 * count * 4, cudaMemcpyHostToDevice, c->stream));
         k_unpack_queries<<<c->num_sms * 4, 256, 0, c->stream>>>(
-            c->dp, reinterpret_cast<const uint8_t*>(c->h2d_stage.p), d_off.p, d_slots.p,
+            dparams(c), reinterpret_cast<const uint8_t*>(c->h2d_stage.p), d_off.p, d_slots.p,
             d_slots.p + count, count, l, c->pool_n.p);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(c->stream));  // host vectors and temporaries go out of scope
@@ -1223,7 +1262,7 @@ int locpir_b200_pool_load_zero_sheet(locpir_b200_ctx* c, const uint8_t* payload,
         d_val.reserve(regions, c->stream, false);
         CK(cudaMemcpyAsync(c->h2d_stage.p, payload, len, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(d_val.p, service_values, regions * 8ull, cudaMemcpyHostToDevice, c->stream));
-        k_load_zero_sheet<<<c->num_sms * 4, 256, 0, c->stream>>>(c->dp, c->h2d_stage.p, d_val.p, bits,
+        k_load_zero_sheet<<<c->num_sms * 4, 256, 0, c->stream>>>(dparams(c), c->h2d_stage.p, d_val.p, bits,
                                                                regions, svc_first, c->pool_n.p);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(c->stream));
@@ -1246,7 +1285,7 @@ int locpir_b200_pool_store_responses(locpir_b200_ctx* c, const uint32_t* out_fir
         DevBuf<uint32_t> d_first;
         d_first.reserve(count, c->stream, false);
         CK(cudaMemcpyAsync(d_first.p, out_first, count * 4, cudaMemcpyHostToDevice, c->stream));
-        k_pack_responses<<<c->num_sms * 4, 256, 0, c->stream>>>(c->dp, c->pool_n.p, d_first.p, count,
+        k_pack_responses<<<c->num_sms * 4, 256, 0, c->stream>>>(dparams(c), c->pool_n.p, d_first.p, count,
                                                               m, c->d2h_stage.p);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(payloads, c->d2h_stage.p, words * 4, cudaMemcpyDeviceToHost, c->stream));
@@ -1416,7 +1455,7 @@ int locpir_b200_client_encrypt(locpir_b200_ctx* c, const uint8_t* lwe_key, uint6
         CK(cudaMemcpyAsync(d_key.p, lwe_key, c->p.n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(d_mu.p, mus, count * 4, cudaMemcpyHostToDevice, c->stream));
         const uint64_t blocks = std::min<uint64_t>((count + 7) / 8, (uint64_t)c->num_sms * 16);
-        k_client_encrypt<<<(unsigned)blocks, 256, 0, c->stream>>>(c->dp, d_key.p, seed, first_index,
+        k_client_encrypt<<<(unsigned)blocks, 256, 0, c->stream>>>(dparams(c), d_key.p, seed, first_index,
                                                                 d_mu.p, count, c->p.alpha_in,
                                                                 first_slot, c->pool_n.p);
         CK(cudaGetLastError());
@@ -1445,7 +1484,7 @@ int locpir_b200_debug_fft_error(locpir_b200_ctx* c, const uint32_t* lwe_n, uint6
         for (uint64_t g = 0; g < count; g++)
             items[g] = {(uint32_t)g, SLOT_NONE, 1, 0, 0u, (uint32_t)g, SLOT_NONE, 0};
         if (count > c->scratch_slots) {
-            c->pool_N.reserve((size_t)count * c->dp.N_stride, c->stream, false);
+            grow_scratch(c, count);
             c->scratch_slots = c->pool_N.n / c->dp.N_stride;
         }
         DevBuf<BrItem> d;
@@ -1457,10 +1496,10 @@ int locpir_b200_debug_fft_error(locpir_b200_ctx* c, const uint32_t* lwe_n, uint6
         const uint32_t mu = 0x20000000u;
         if (c->p.bk_l == 3 && c->p.bk_bgbit == 7)
             k_blind_rotate<3, 7, true><<<(unsigned)count, 64, 0, c->stream>>>(
-                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, tabs(c), mu, e.p);
+                dparams(c), d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, tabs(c), mu, e.p);
         else if (c->p.bk_l == 2 && c->p.bk_bgbit == 10)
             k_blind_rotate<2, 10, true><<<(unsigned)count, 64, 0, c->stream>>>(
-                c->dp, d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, tabs(c), mu, e.p);
+                dparams(c), d.p, c->pool_n.p, c->pool_N.p, c->bkf.p, tabs(c), mu, e.p);
         else
             throw std::invalid_argument("no blind-rotate kernel instantiated for this (l, Bgbit)");
         CK(cudaGetLastError());

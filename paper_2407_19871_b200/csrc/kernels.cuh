@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cassert>
+
 #include "fft.cuh"
 #include "cbrng.h"
 
@@ -52,7 +54,55 @@ struct DevParams {
     uint32_t n, N, l, bgbit, t, basebit;
     uint32_t n_stride;  // padded n+1
     uint32_t N_stride;  // padded N+1
+    uint64_t pool_slots, scratch_slots;  // current pool sizes (bounds for LPB_CHECKS)
 };
+
+// ---- self-check build (compute-sanitizer is closed on the GPU pool):
+//   LPB_CHECKS=1  device asserts on every pool / scratch / table index a kernel forms
+//   LPB_JITTER=1  a pseudo-random __nanosleep before every barrier and warp sync, so a
+//                 missing or misplaced barrier shows up as a result that changes from run
+//                 to run (tools/selfcheck.sh compares digests across runs and poisons)
+#ifndef LPB_CHECKS
+#define LPB_CHECKS 0
+#endif
+#ifndef LPB_JITTER
+#define LPB_JITTER 0
+#endif
+#if LPB_CHECKS
+#define LPB_ASSERT(x) assert(x)
+#else
+#define LPB_ASSERT(x) ((void)0)
+#endif
+__constant__ uint32_t c_poison;  // LOCPIR_B200_POISON (checked build: shared memory poison)
+
+__global__ void k_fill(uint32_t* __restrict__ p, size_t words, uint32_t v)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words;
+         i += (size_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// checked build: fill this CTA's shared memory with the poison word before use
+__device__ __forceinline__ void lpb_poison_smem(void* base, size_t bytes)
+{
+#if LPB_CHECKS
+    uint32_t* w = reinterpret_cast<uint32_t*>(base);
+    for (size_t i = threadIdx.x; i < bytes / 4; i += blockDim.x)
+        w[i] = c_poison;
+    __syncthreads();
+#else
+    (void)base;
+    (void)bytes;
+#endif
+}
+
+__device__ __forceinline__ void lpb_jitter()
+{
+#if LPB_JITTER
+    unsigned s = (unsigned)clock() * 2654435761u ^ (threadIdx.x * 0x9E3779B9u) ^ blockIdx.x;
+    __nanosleep((s >> 20) & 511u);
+#endif
+}
 
 // The transform's device tables (engine.cu make_tables; same values as the oracle's
 // or_fft2_make_tables): per-thread forward / inverse twiddles [8][64] and the factored
@@ -103,7 +153,10 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
 constexpr int MAX_N = 639;
 constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BR_MIN_BLOCKS
-#define BR_MIN_BLOCKS 4
+#define BR_MIN_BLOCKS 4  // ciphertexts resident per SM (255 registers per thread)
+#endif
+#ifndef BK_PREFETCH
+#define BK_PREFETCH 0    // 1: BK rows loaded one transform ahead (round 1; 629 vs 617 ms measured in round 2)
 #endif
 
 __device__ __forceinline__ uint32_t rot_read(const uint32_t* p, uint32_t a, int j)
@@ -157,6 +210,14 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
     const uint32_t n = dp.n;
+    LPB_ASSERT(it.in0 < dp.pool_slots && it.out < dp.scratch_slots);
+    LPB_ASSERT((it.in1 == SLOT_NONE || it.in1 < dp.pool_slots) &&
+               (it.in2 == SLOT_NONE || it.in2 < dp.pool_slots) && n <= MAX_N);
+#if LPB_CHECKS
+    lpb_poison_smem(acc, sizeof(acc));
+    lpb_poison_smem(xbuf, sizeof(xbuf));
+    lpb_poison_smem(abar, sizeof(abar));
+#endif
 
     // ---- prologue: gate linear form (gate_engine.hpp:196-269) + mod switch to [0, 2N)
     {
@@ -186,8 +247,14 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     }
     const FwdTw tw = load_fwd_tw(tb.fwd, t);
     const double2 twt = tb.tw[t];  // psi^t (untwist factors formed on the fly)
-    auto bar = [] { __syncthreads(); };
-    auto wbar = [] { __syncwarp(); };
+    auto bar = [] {
+        lpb_jitter();
+        __syncthreads();
+    };
+    auto wbar = [] {
+        lpb_jitter();
+        __syncwarp();
+    };
     int xs = 0;  // alternating cross-warp tile
 
     constexpr uint32_t HALF = 1u << (BGBIT - 1);
@@ -200,8 +267,10 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 
     constexpr int ROWS = 2 * L;
     for (uint32_t i = 0; i < n; i++) {
+        lpb_jitter();
         __syncthreads();
         const uint32_t a = abar[i];
+        LPB_ASSERT(a < 2048u);
         if (a == 0)
             continue;
         double2 oA[8], oB[8];
@@ -225,12 +294,14 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 // prefetch this row's BK slots; the loads land while the transform runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
                 double2 BA[8], BB[8];
+#if BK_PREFETCH
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BA[q] = ld_stream(row + q * 64 + t);
 #pragma unroll
                 for (int q = 0; q < 8; q++)
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
+#endif
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
 #pragma unroll
@@ -241,6 +312,13 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 }
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
+#if !BK_PREFETCH
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    BA[q] = ld_stream(row + q * 64 + t);
+                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
+                }
+#endif
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     mac(oA[q], x[q], BA[q]);
@@ -322,6 +400,8 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
         uint16_t d = 0;
         if (c < nct) {
             const KsItem it = items[first + c];
+            LPB_ASSERT(it.in0 < dp.scratch_slots && it.out < dp.pool_slots &&
+                       (it.in1 == SLOT_NONE || it.in1 < dp.scratch_slots));
             uint32_t v = pool_N[(size_t)it.in0 * dp.N_stride + i];
             if (it.in1 != SLOT_NONE)
                 v += pool_N[(size_t)it.in1 * dp.N_stride + i];
@@ -416,6 +496,7 @@ __global__ void k_linear(DevParams dp, const LinItem* __restrict__ items, uint32
          e += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t g = (uint32_t)(e / words), w = (uint32_t)(e - (uint64_t)g * words);
         const LinItem it = items[g];
+        LPB_ASSERT(it.out < dp.pool_slots && (it.kind == 2 || it.in0 < dp.pool_slots));
         uint32_t v;
         if (it.kind == 2)
             v = w == dp.n ? it.in0 : 0u;
@@ -587,6 +668,7 @@ __global__ void __launch_bounds__(KS_THREADS)
 {
     const uint32_t g = blockIdx.x, split = blockIdx.y;
     const KsItem it = items[g];
+    LPB_ASSERT(it.in0 < dp.scratch_slots && (it.in1 == SLOT_NONE || it.in1 < dp.scratch_slots));
     const uint32_t N = dp.N, per = N / KS_SPLIT;
     const uint32_t prec = 1u << (32 - (1 + dp.basebit * dp.t));
     const uint32_t col = threadIdx.x * KS_COLS;
@@ -624,6 +706,7 @@ __global__ void __launch_bounds__(KS_THREADS)
 {
     const uint32_t g = blockIdx.x;
     const KsItem it = items[g];
+    LPB_ASSERT(it.out < dp.pool_slots);
     for (uint32_t col = threadIdx.x; col < dp.n_stride; col += blockDim.x) {
         uint32_t v = 0;
         if (col == dp.n) {
@@ -654,6 +737,7 @@ constexpr size_t kLatSmemBytes = sizeof(LatSmem<L>);
 
 __device__ __forceinline__ void group_bar(int id)
 {
+    lpb_jitter();
     asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory");
 }
 
@@ -668,6 +752,8 @@ __global__ void __launch_bounds__(128 * L, 1)
     const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
     const BrItem it = items[blockIdx.x];
     const uint32_t n = dp.n;
+    LPB_ASSERT(it.in0 < dp.pool_slots && it.out < dp.scratch_slots && n <= MAX_N);
+    lpb_poison_smem(smem_l, sizeof(LatSmem<L>));
     {
         const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
         const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
