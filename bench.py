@@ -42,15 +42,20 @@ def flop_per_br(n=630, k=1, l=3, N=1024):
     return n * (((k + 1) * l + (k + 1)) * F_FFT + (k + 1) ** 2 * l * (N // 2) * 8)
 
 
+TRAFFIC_FILES = ("r02_traffic.json", "r01_traffic.json")  # newest committed capture first
+
+
 def committed_traffic(kernel="k_blind_rotate<3, 7>"):
     """dram__bytes_read.sum + dram__bytes_write.sum of one full-size launch, from the
-    committed ncu capture (profiles/r01_traffic.json); None when absent."""
-    try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))
-        k = d["kernels"][kernel]
-        return k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
-    except Exception:
-        return None
+    newest committed ncu capture (profiles/r0N_traffic.json); None when absent."""
+    for f in TRAFFIC_FILES:
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", f)))
+            k = d["kernels"][kernel]
+            return k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
+        except Exception:
+            continue
+    return None
 
 
 def locpir_roofline(sec, units_per_query, qps, n_gpus, peak_tflops):
@@ -84,12 +89,7 @@ def keyswitch_view(G, params, avg_ks_ms, ksk_bytes):
     secs = avg_ks_ms * 1e-3
     adds = G * params.N * params.c.ks_t * (params.n + 1) * 0.75
     int_peak = 148 * 128 * 1.965e9
-    dram = None
-    try:
-        k = json.load(open(os.path.join(ROOT, "profiles", "r01_traffic.json")))["kernels"]["k_keyswitch"]
-        dram = (k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]) if G == GATES_PER_GPU else None
-    except Exception:
-        pass
+    dram = committed_traffic("k_keyswitch") if G == GATES_PER_GPU else None
     try:
         hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
@@ -772,8 +772,8 @@ def run_b200(args):
                 "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved_tflops / peak if peak else None,
                 "traffic": committed_traffic() if G == GATES_PER_GPU else None,
-                "traffic_unit": "bytes per launch (DRAM read+write, ncu capture in "
-                                "profiles/r01_traffic.json)",
+                "traffic_unit": "bytes per launch (DRAM read+write, the newest ncu capture "
+                                "in profiles/r0N_traffic.json)",
                 "algorithmic_bytes_per_launch": G * (2 * 4 * (params.n + 1) + 4 * (params.N + 1))
                                                 + params.bk_words() * 8,
                 "flop_per_unit": flop_per_br(), "units_per_launch": G,

@@ -271,10 +271,6 @@ Tables make_tables(uint32_t N)
             T.inv[e * 64 + t] = g[e];
         }
     }
-    // compact pass-1 table [e][k] (k = t >> 3), read at use under FWD_TW1_MEM
-    for (int e = 0; e < 4; e++)
-        for (int k = 0; k < 8; k++)
-            T.fwd.push_back(T.fwd[e * 64 + 8 * k]);
     T.fwd0[0] = node[1];
     T.fwd0[1] = node[2];
     T.fwd0[2] = node[4];

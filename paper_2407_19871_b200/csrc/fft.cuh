@@ -271,31 +271,13 @@ __device__ __forceinline__ void exch_p1_to_p2(double2 x[8], double2* buf, int t,
 // (pass-2 layout).  bufX: cross-warp exchange tile (needs the 64-thread barrier `bar`);
 // bufW: intra-warp exchange tile (after tree stage 0 the two 256-point halves are
 // independent and warp w owns half w in passes 1 and 2, so `wbar` = __syncwarp).
-// FWD_TW1_MEM (A/B switch): the pass-1 twiddles (they depend on k = t >> 3 only) are read
-// at use from the compact table T1[e][k] (4 distinct addresses per warp: one broadcast
-// wavefront per load) instead of being held in 16 registers for the whole kernel.
-#ifndef FWD_TW1_MEM
-#define FWD_TW1_MEM 0
-#endif
 template <class Bar, class WBar>
 __device__ __forceinline__ void fft_forward(double2 x[8], const FwdTw& tw, double2* bufX,
-                                            double2* bufW, int t, Bar bar, WBar wbar,
-                                            const double2* __restrict__ T1 = nullptr)
+                                            double2* bufW, int t, Bar bar, WBar wbar)
 {
     fwd_pass0(x);
     exch_p0_to_p1(x, bufX, t, bar);
-#if FWD_TW1_MEM
-    if (T1) {
-        FwdTw w = tw;
-        const int k = t >> 3;
-        w.s3 = __ldg(T1 + 0 * 8 + k);
-        w.s4 = __ldg(T1 + 1 * 8 + k);
-        w.s5a = __ldg(T1 + 2 * 8 + k);
-        w.s5b = __ldg(T1 + 3 * 8 + k);
-        fwd_pass1(x, w);
-    } else
-#endif
-        fwd_pass1(x, tw);
+    fwd_pass1(x, tw);
     exch_p1_to_p2(x, bufW, t, wbar);
     fwd_pass2(x, tw);
 }

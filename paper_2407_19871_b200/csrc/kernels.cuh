@@ -155,10 +155,6 @@ constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4  // ciphertexts resident per SM (255 registers per thread)
 #endif
-#ifndef K1_PUNROLL
-#define K1_PUNROLL 1     // digit-loop unroll in K1 (A/B knob)
-#endif
-constexpr int kPUnroll = K1_PUNROLL;
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 0    // 1: BK rows loaded one transform ahead (round 1; 629 vs 617 ms measured in round 2)
 #endif
@@ -293,7 +289,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 tmp[q] = rot_read(acc[c], a, j) - acc[c][j] + OFF;
                 tmp[8 + q] = rot_read(acc[c], a, j + 512) - acc[c][j + 512] + OFF;
             }
-#pragma unroll kPUnroll
+#pragma unroll 1
             for (int p = 0; p < L; p++) {
                 // prefetch this row's BK slots; the loads land while the transform runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
@@ -314,7 +310,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
                     x[q] = make_double2((double)dlo, (double)dhi);
                 }
-                fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar, tb.fwd + 8 * 64);
+                fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
 #if !BK_PREFETCH
 #pragma unroll

@@ -3,9 +3,9 @@
 # K1/K2.  Every ncu pass runs only after the same command exited 0 without ncu.
 set -x
 make -s -C paper_2407_19871_b200/csrc > /dev/null
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/e_gpu_tests.log 2>&1; echo tests=$? > gpurun_out/e_status.txt
-timeout 900 python bench.py > gpurun_out/e_bench.json 2> gpurun_out/e_bench.err; echo bench=$? >> gpurun_out/e_status.txt
-timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/e_ref.json 2> gpurun_out/e_ref.err; echo ref=$? >> gpurun_out/e_status.txt
+timeout 1800 python -m pytest tests -m gpu -q -s > gpurun_out/e_gpu_tests.log 2>&1; echo tests=$? > gpurun_out/e_status.txt
+timeout 2400 python bench.py > gpurun_out/e_bench.json 2> gpurun_out/e_bench.err; echo bench=$? >> gpurun_out/e_status.txt
+timeout 1200 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/e_ref.json 2> gpurun_out/e_ref.err; echo ref=$? >> gpurun_out/e_status.txt
 B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-locpir"
 timeout 600 $B > gpurun_out/e_plain.json 2>&1 && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \

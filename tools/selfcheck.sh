@@ -5,6 +5,7 @@
 mkdir -p gpurun_out
 OUT=gpurun_out/selfcheck.txt
 : > $OUT
+make -s -C paper_2407_19871_b200/csrc variant V=checked DEFS="-DLPB_CHECKS=1 -DLPB_JITTER=1" > /dev/null 2>&1
 CHECKED=$PWD/paper_2407_19871_b200/lib_checked.so
 for level in 128 80; do
   for small in 1 0; do

@@ -12,14 +12,17 @@ G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 
 
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
+
+
 def main():
-    d = json.load(open(os.path.join(G, "e_bench.json")))
+    d = json.loads(open(os.path.join(G, "e_bench.json")).read().strip().splitlines()[-1])
     loc = {k: d.pop(k) for k in ("locpir", "cpu_baseline_locpir", "reference_standin_locpir") if k in d}
-    json.dump(d, open(os.path.join(P, "r01_bench_b200.json"), "w"), indent=1)
-    json.dump(loc, open(os.path.join(P, "r01_bench_b200_locpir.json"), "w"), indent=1)
-    json.dump(json.load(open(os.path.join(G, "e_ref.json"))),
-              open(os.path.join(P, "r01_bench_reference.json"), "w"), indent=1)
-    for src, dst in (("e_launches.csv", "r01_launches.csv"), ("e_gpu_tests.log", "r01_gpu_tests.log")):
+    json.dump(d, open(os.path.join(P, f"{TAG}_bench_b200.json"), "w"), indent=1)
+    json.dump(loc, open(os.path.join(P, f"{TAG}_bench_b200_locpir.json"), "w"), indent=1)
+    json.dump(json.loads(open(os.path.join(G, "e_ref.json")).read().strip().splitlines()[-1]),
+              open(os.path.join(P, f"{TAG}_bench_reference.json"), "w"), indent=1)
+    for src, dst in (("e_launches.csv", f"{TAG}_launches.csv"), ("e_gpu_tests.log", f"{TAG}_gpu_tests.log")):
         open(os.path.join(P, dst), "w").write(open(os.path.join(G, src)).read())
     rows = list(csv.reader(open(os.path.join(G, "e_traffic.csv"))))
     hdr, ks = None, {}
@@ -31,11 +34,16 @@ def main():
             x = dict(zip(hdr, r))
             key = "k_blind_rotate<3, 7>" if "blind_rotate" in x["Kernel Name"] else "k_keyswitch"
             ks.setdefault(key, {})[x["Metric Name"]] = float(x["Metric Value"].replace(",", ""))
-    t = json.load(open(os.path.join(P, "r01_traffic.json")))
-    t["kernels"] = ks
-    json.dump(t, open(os.path.join(P, "r01_traffic.json"), "w"), indent=1)
-    for rep, out, title in (("e_prof_br", "r01_ncu_blind_rotate.txt", "^k_blind_rotate$"),
-                            ("e_prof_ks", "r01_ncu_keyswitch.txt", "^k_keyswitch$")):
+    t = {"what": "DRAM bytes read + written and L2 hit rate per launch, steady state (the first "
+                 "two launches skipped), cfg2 full size (65,536 gates)",
+         "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
+                    "gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none "
+                    "-k regex:'^k_blind_rotate$|^k_keyswitch$' --launch-skip 2 -c 2 python "
+                    "bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-locpir",
+         "kernels": ks}
+    json.dump(t, open(os.path.join(P, f"{TAG}_traffic.json"), "w"), indent=1)
+    for rep, out, title in (("e_prof_br", f"{TAG}_ncu_blind_rotate.txt", "^k_blind_rotate$"),
+                            ("e_prof_ks", f"{TAG}_ncu_keyswitch.txt", "^k_keyswitch$")):
         r = os.path.join(G, rep + ".ncu-rep")
         summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), r],
                               capture_output=True, text=True).stdout
