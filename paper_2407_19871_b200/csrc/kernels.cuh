@@ -376,6 +376,9 @@ constexpr int kKsJUnroll = KS_JUNROLL;  // digit-position loop unrolling (icache
 #ifndef KS_MINB
 #define KS_MINB 4
 #endif
+#ifndef KS_PAIRS
+#define KS_PAIRS 0
+#endif
 #ifndef KS_CT_DEF
 #define KS_CT_DEF 16
 #endif
@@ -436,6 +439,54 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
     const size_t row_stride = dp.n_stride;
     const uint4* base = reinterpret_cast<const uint4*>(ksk + col);
     const size_t rs4 = row_stride / 4;
+#if KS_PAIRS
+    // Two digit positions (j, j+1) per step: the 4-bit digit pair of each ciphertext picks
+    // one of 16 cases (warp-uniform: every lane serves the same ciphertext), each a
+    // 3-input add (acc - row_a - row_b) -- half the adds and half the branches.
+    auto sub1 = [](uint4& a, const uint4& r) {
+        a.x -= r.x; a.y -= r.y; a.z -= r.z; a.w -= r.w;
+    };
+    auto sub2 = [](uint4& a, const uint4& r, const uint4& s) {
+        a.x = a.x - r.x - s.x; a.y = a.y - r.y - s.y; a.z = a.z - r.z - s.z; a.w = a.w - r.w - s.w;
+    };
+    for (uint32_t i = 0; i < N; i++) {
+        uint32_t dw[KS_CT / 2];
+        const uint32_t* dp32 = reinterpret_cast<const uint32_t*>(dig + i * KS_CT);
+#pragma unroll
+        for (int c = 0; c < KS_CT / 2; c++)
+            dw[c] = dp32[c];
+#pragma unroll 1
+        for (int jp = 0; jp < 4; jp++) {
+            const uint4* ra = base + ((size_t)i * 24 + (2 * jp) * 3) * rs4;
+            const uint4* rb = ra + 3 * rs4;
+            const uint4 a1 = __ldg(ra), a2 = __ldg(ra + rs4), a3 = __ldg(ra + 2 * rs4);
+            const uint4 b1 = __ldg(rb), b2 = __ldg(rb + rs4), b3 = __ldg(rb + 2 * rs4);
+            const int sh = 12 - 4 * jp;
+#pragma unroll
+            for (int c = 0; c < KS_CT; c++) {
+                const uint32_t w = dw[c >> 1] >> ((c & 1) * 16);
+                switch ((w >> sh) & 15u) {  // (d_j << 2) | d_{j+1}
+                case 1: sub1(acc[c], b1); break;
+                case 2: sub1(acc[c], b2); break;
+                case 3: sub1(acc[c], b3); break;
+                case 4: sub1(acc[c], a1); break;
+                case 5: sub2(acc[c], a1, b1); break;
+                case 6: sub2(acc[c], a1, b2); break;
+                case 7: sub2(acc[c], a1, b3); break;
+                case 8: sub1(acc[c], a2); break;
+                case 9: sub2(acc[c], a2, b1); break;
+                case 10: sub2(acc[c], a2, b2); break;
+                case 11: sub2(acc[c], a2, b3); break;
+                case 12: sub1(acc[c], a3); break;
+                case 13: sub2(acc[c], a3, b1); break;
+                case 14: sub2(acc[c], a3, b2); break;
+                case 15: sub2(acc[c], a3, b3); break;
+                default: break;
+                }
+            }
+        }
+    }
+#else
 #if KS_PREFETCH
     uint4 n1 = __ldg(base), n2 = __ldg(base + rs4), n3 = __ldg(base + 2 * rs4);
 #endif
@@ -475,6 +526,7 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
             }
         }
     }
+#endif  // KS_PAIRS
 #pragma unroll
     for (int c = 0; c < KS_CT; c++) {
         if ((uint32_t)c < nct) {

@@ -123,6 +123,70 @@ class ClientKeys:
             _u32(self.bk) if evaluation_keys else None,
             _u32(self.ksk) if evaluation_keys else None))
 
+    # ---- key blobs (SURVEY §5 "persist BK/KSK blobs (torus form) to skip keygen") -------
+    _MAGIC = b"LOCPIRB200KEYS\x00\x01"
+
+    def save(self, path: str, secret: bool = True):
+        """Write the key set to `path`: a header (magic, the 9 parameters), the LWE and
+        TRLWE keys (omitted with secret=False: a server-side evaluation-key file), BK and
+        KSK in torus form, and a SHA-256 over everything before it."""
+        import hashlib
+        import struct
+        p = self.params.c
+        hdr = self._MAGIC + struct.pack("<7I2d?", p.n, p.N, p.k, p.bk_l, p.bk_bgbit, p.ks_t,
+                                        p.ks_basebit, p.alpha_in, p.alpha_bk, bool(secret))
+        parts = [hdr]
+        if secret:
+            parts += [self.lwe_key.tobytes(), self.trlwe_key.tobytes()]
+        if self.bk is None:
+            raise LogicError("no evaluation keys to save")
+        parts += [self.bk.astype("<u4").tobytes(), self.ksk.astype("<u4").tobytes()]
+        body = b"".join(parts)
+        with open(path, "wb") as f:
+            f.write(body + hashlib.sha256(body).digest())
+
+    @classmethod
+    def load(cls, path: str) -> "ClientKeys":
+        """Read a key file written by save(); raises InvalidArgument on a bad magic, an
+        unknown parameter set, a truncated file or a checksum mismatch."""
+        import hashlib
+        import struct
+        raw = open(path, "rb").read()
+        m = cls._MAGIC
+        fmt = "<7I2d?"
+        hl = len(m) + struct.calcsize(fmt)
+        if len(raw) < hl + 32 or raw[:len(m)] != m:
+            raise InvalidArgument(f"{path}: not a locpir_b200 key file")
+        body, digest = raw[:-32], raw[-32:]
+        if hashlib.sha256(body).digest() != digest:
+            raise InvalidArgument(f"{path}: checksum mismatch")
+        n, N, k, l, bg, t, bb, ain, abk, secret = struct.unpack(fmt, raw[len(m):hl])
+        params = None
+        for level in (128, 80):
+            q = TfheParams(level)
+            c = q.c
+            if (c.n, c.N, c.k, c.bk_l, c.bk_bgbit, c.ks_t, c.ks_basebit, c.alpha_in,
+                    c.alpha_bk) == (n, N, k, l, bg, t, bb, ain, abk):
+                params = q
+        if params is None:
+            raise InvalidArgument(f"{path}: parameter set is not a BASELINE set")
+        keys = cls.__new__(cls)
+        keys.params = params
+        off = hl
+        want = (n + N if secret else 0) + 4 * (params.bk_words() + params.ksk_words())
+        if len(body) - hl != want:
+            raise InvalidArgument(f"{path}: truncated key file")
+        if secret:
+            keys.lwe_key = np.frombuffer(body, np.uint8, n, off).copy()
+            keys.trlwe_key = np.frombuffer(body, np.uint8, N, off + n).copy()
+            off += n + N
+        else:
+            keys.lwe_key = keys.trlwe_key = None
+        keys.bk = np.frombuffer(body, "<u4", params.bk_words(), off).astype(np.uint32)
+        off += 4 * params.bk_words()
+        keys.ksk = np.frombuffer(body, "<u4", params.ksk_words(), off).astype(np.uint32)
+        return keys
+
     def encrypt_bits(self, bits, seed: int) -> np.ndarray:
         bits = np.ascontiguousarray(np.asarray(bits, np.uint8).reshape(-1))
         out = np.zeros((len(bits), self.params.n + 1), np.uint32)

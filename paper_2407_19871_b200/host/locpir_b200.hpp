@@ -337,7 +337,15 @@ private:
 // ---- circuits (circuits.hpp:187-324) -------------------------------------------
 struct CipherWord {
     std::vector<CipherBit> bits;  // index 0 = LSB (codec.hpp:106-109)
+    // FixedPointFormat (codec.hpp:16-30); int_bits = frac_bits = 0 leaves it unspecified
+    // (then only the length is compared)
+    uint8_t int_bits = 0, frac_bits = 0;
 };
+
+inline bool same_format(const CipherWord& a, const CipherWord& b)
+{
+    return a.bits.size() == b.bits.size() && a.int_bits == b.int_bits && a.frac_bits == b.frac_bits;
+}
 
 struct ServiceCiphertext {
     std::vector<CipherBit> bits;
@@ -357,7 +365,7 @@ struct BatchScope {
 
 inline CipherBit hom_less(const CipherWord& a, const CipherWord& b, GateEngine& e)
 {
-    if (a.bits.size() != b.bits.size())
+    if (!same_format(a, b))
         throw std::invalid_argument("comparator operands must share length and format");
     if (a.bits.empty())
         throw std::invalid_argument("comparator operands must be non-empty");
@@ -430,7 +438,7 @@ inline ServiceCiphertext xor_sum_services(const std::vector<ServiceCiphertext>& 
 // borrow_{i+1} = MAJ(NOT a'_i, b'_i, borrow_i): l bootstraps instead of 3l.
 inline CipherBit hom_less_maj(const CipherWord& a, const CipherWord& b, GateEngine& e)
 {
-    if (a.bits.size() != b.bits.size() || a.bits.empty())
+    if (!same_format(a, b) || a.bits.empty())
         throw std::invalid_argument("comparator operands must share length and format");
     BatchScope scope(e);
     const size_t l = a.bits.size();
@@ -452,6 +460,17 @@ inline ServiceCiphertext loc_pir(const CipherWord& x, const CipherWord& y,
 {
     if (regions.empty())
         return {};
+    // the reference's argument checks (circuits.hpp:283-292)
+    if (!same_format(x, y))
+        throw std::invalid_argument("coordinate words must share a format");
+    const size_t m = regions[0].service.bits.size();
+    for (const EncodedRegion& r : regions) {
+        if (!same_format(r.x1, x) || !same_format(r.x2, x) || !same_format(r.y1, y) ||
+            !same_format(r.y2, y))
+            throw std::invalid_argument("region boundary format mismatch");
+        if (r.service.bits.size() != m)
+            throw std::invalid_argument("regions must share the service bit-length");
+    }
     BatchScope scope(e);
     auto lt = [&](const CipherWord& a, const CipherWord& b) {
         return cmp == Comparator::Majority ? hom_less_maj(a, b, e) : hom_less(a, b, e);

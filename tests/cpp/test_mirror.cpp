@@ -178,6 +178,20 @@ int main()
             CHECK(dec_service(loc_pir(x, y, regions, eng, true, Comparator::Majority), eng) == want);
         }
         CHECK(eng.counters().bootstrap_units() == 8 * N * (4 * l + 2 * m + 3));
+        // the reference's argument checks (circuits.hpp:283-292)
+        {
+            const CipherWord x = enc_int(1, l, eng), y = enc_int(2, l, eng);
+            CipherWord y13 = y;
+            y13.int_bits = 9;
+            y13.frac_bits = 4;
+            CHECK_THROWS_AS(loc_pir(x, y13, regions, eng), std::invalid_argument);
+            auto bad = regions;
+            bad[1].service.bits.pop_back();
+            CHECK_THROWS_AS(loc_pir(x, y, bad, eng), std::invalid_argument);
+            bad = regions;
+            bad[0].x2.bits.pop_back();
+            CHECK_THROWS_AS(loc_pir(x, y, bad, eng), std::invalid_argument);
+        }
     }
 
     // majority gate truth table (one bootstrap of a + b + c)

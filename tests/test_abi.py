@@ -177,3 +177,31 @@ def test_ctx_rejects_parameters_the_kernels_are_not_built_for():
         h = C.c_void_p()
         assert L.locpir_b200_ctx_create(C.byref(p), 0, None, C.byref(h)) == _abi.EINVAL
         assert not h.value
+
+
+def test_key_blob_roundtrip(tmp_path):
+    """BK/KSK blobs persisted in torus form (skip keygen); secret-less server
+    files; tampering and truncation are rejected."""
+    from paper_2407_19871_b200 import ClientKeys, TfheParams
+    from paper_2407_19871_b200.engine import InvalidArgument
+    k = ClientKeys(TfheParams(80), 5)
+    f = tmp_path / "k.bin"
+    k.save(str(f))
+    r = ClientKeys.load(str(f))
+    assert r.params.security_bits == 80
+    for a in ("lwe_key", "trlwe_key", "bk", "ksk"):
+        assert np.array_equal(getattr(r, a), getattr(k, a))
+    bits = np.array([1, 0, 1], np.uint8)
+    assert list(r.decrypt_bits(k.encrypt_bits(bits, 3))) == list(bits)
+    pub = tmp_path / "pub.bin"
+    k.save(str(pub), secret=False)
+    p = ClientKeys.load(str(pub))
+    assert p.lwe_key is None and np.array_equal(p.bk, k.bk)
+    raw = bytearray(f.read_bytes())
+    raw[100] ^= 1
+    f.write_bytes(bytes(raw))
+    with pytest.raises(InvalidArgument, match="checksum"):
+        ClientKeys.load(str(f))
+    f.write_bytes(b"junk")
+    with pytest.raises(InvalidArgument, match="not a locpir_b200 key file"):
+        ClientKeys.load(str(f))
