@@ -155,6 +155,9 @@ constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4  // ciphertexts resident per SM (255 registers per thread)
 #endif
+#ifndef BK_SPLIT
+#define BK_SPLIT 0       // A/B: BK loads split across the transform (see K1)
+#endif
 #ifndef BK_PREFETCH
 #define BK_PREFETCH 0    // 1: BK rows loaded one transform ahead (round 1; 629 vs 617 ms measured in round 2)
 #endif
@@ -310,9 +313,32 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
                     x[q] = make_double2((double)dlo, (double)dhi);
                 }
+#if BK_SPLIT
+                // split prefetch: BA issued early (BK_SPLIT 1: before the transform,
+                // 2: after the cross-warp exchange), BB after the intra-warp exchange
+#if BK_SPLIT == 1
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    BA[q] = ld_stream(row + q * 64 + t);
+#endif
+                fwd_pass0(x);
+                exch_p0_to_p1(x, xbuf[xs], t, bar);
+#if BK_SPLIT == 2
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    BA[q] = ld_stream(row + q * 64 + t);
+#endif
+                fwd_pass1(x, tw);
+                exch_p1_to_p2(x, xbuf[2], t, wbar);
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
+                fwd_pass2(x, tw);
+#else
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
+#endif
                 xs ^= 1;
-#if !BK_PREFETCH
+#if !BK_PREFETCH && !BK_SPLIT
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     BA[q] = ld_stream(row + q * 64 + t);
