@@ -195,6 +195,55 @@ __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
     acc.y = im;
 }
 
+// ---- ACC_TMEM (A/B knob): the frequency-domain accumulators live in tensor memory
+// (64 TMEM columns per CTA, each thread its own lane) instead of 64 registers, so that
+// 6 CTAs (12 warps) fit per SM.  tcgen05.ld / .st move 16 words per thread at a time.
+#ifndef ACC_TMEM
+#define ACC_TMEM 0
+#endif
+__device__ __forceinline__ void tmem_ld16x2(uint32_t a0, uint32_t a1, uint32_t (&v)[16],
+                                            uint32_t (&w)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15}, [%16];\n"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(a0));
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15}, [%16];\n"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+          "=r"(w[14]), "=r"(w[15])
+        : "r"(a1));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};\n"
+        :
+        : "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+          "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
+          "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ double2 unpack2(const uint32_t* v)
+{
+    return make_double2(__hiloint2double((int)v[1], (int)v[0]), __hiloint2double((int)v[3], (int)v[2]));
+}
+__device__ __forceinline__ void pack2(uint32_t* v, double2 d)
+{
+    v[0] = (uint32_t)__double2loint(d.x);
+    v[1] = (uint32_t)__double2hiint(d.x);
+    v[2] = (uint32_t)__double2loint(d.y);
+    v[3] = (uint32_t)__double2hiint(d.y);
+}
+
 // ERR = true (diagnostic instantiation only): also record max |w - rint(w)| over every
 // inverse-transform output before rounding -- the FFT rounding margin (exact iff < 1/2).
 template <int L, int BGBIT, bool ERR = false>
@@ -250,6 +299,18 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     }
     const FwdTw tw = load_fwd_tw(tb.fwd, t);
     const double2 twt = tb.tw[t];  // psi^t (untwist factors formed on the fly)
+#if ACC_TMEM
+    __shared__ uint32_t acc_tslot;
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&acc_tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tacc = acc_tslot + ((uint32_t)(t & 32) << 16);  // this warp's lane quarter
+#endif
     auto bar = [] {
         lpb_jitter();
         __syncthreads();
@@ -276,12 +337,16 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         LPB_ASSERT(a < 2048u);
         if (a == 0)
             continue;
+#if ACC_TMEM
+        bool first = true;
+#else
         double2 oA[8], oB[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             oA[q] = make_double2(0.0, 0.0);
             oB[q] = make_double2(0.0, 0.0);
         }
+#endif
         const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
 #pragma unroll
         for (int c = 0; c < 2; c++) {
@@ -338,20 +403,66 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
 #endif
                 xs ^= 1;
-#if !BK_PREFETCH && !BK_SPLIT
+#if !BK_PREFETCH && !BK_SPLIT && !ACC_TMEM
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     BA[q] = ld_stream(row + q * 64 + t);
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
                 }
 #endif
+#if ACC_TMEM
+                // MAC into the TMEM accumulators, 4 slots (16 words per output) at a time
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+#if !BK_PREFETCH && !BK_SPLIT
+#pragma unroll
+                    for (int qq = 0; qq < 4; qq++) {
+                        BA[4 * h + qq] = ld_stream(row + (4 * h + qq) * 64 + t);
+                        BB[4 * h + qq] = ld_stream(row + FFT_M + (4 * h + qq) * 64 + t);
+                    }
+#endif
+                    uint32_t va[16], vb[16];
+                    if (!first)
+                        tmem_ld16x2(tacc + 16 * h, tacc + 32 + 16 * h, va, vb);
+#pragma unroll
+                    for (int qq = 0; qq < 4; qq++) {
+                        const int q = 4 * h + qq;
+                        double2 oa = first ? make_double2(0.0, 0.0) : unpack2(va + 4 * qq);
+                        double2 ob = first ? make_double2(0.0, 0.0) : unpack2(vb + 4 * qq);
+                        mac(oa, x[q], BA[q]);
+                        mac(ob, x[q], BB[q]);
+                        pack2(va + 4 * qq, oa);
+                        pack2(vb + 4 * qq, ob);
+                    }
+                    tmem_st16(tacc + 16 * h, va);
+                    tmem_st16(tacc + 32 + 16 * h, vb);
+                }
+                tmem_wait_st();
+                first = false;
+#else
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     mac(oA[q], x[q], BA[q]);
                     mac(oB[q], x[q], BB[q]);
                 }
+#endif
             }
         }
+#if ACC_TMEM
+        double2 oA[8], oB[8];
+        {
+            uint32_t va[16], vb[16];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                tmem_ld16x2(tacc + 16 * h, tacc + 32 + 16 * h, va, vb);
+#pragma unroll
+                for (int qq = 0; qq < 4; qq++) {
+                    oA[4 * h + qq] = unpack2(va + 4 * qq);
+                    oB[4 * h + qq] = unpack2(vb + 4 * qq);
+                }
+            }
+        }
+#endif
         // both inverse transforms in lockstep: shared barriers, twice the ILP.  Tiles:
         // intra and cross exchanges alias xbuf[2] / xbuf[xs] (a CTA barrier separates them)
         {
@@ -373,6 +484,13 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j + 512] += (uint32_t)__double2ll_rn(wb.y);
         }
     }
+#if ACC_TMEM
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    if (t < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(acc_tslot));
+#endif
     __syncthreads();
     // ---- sample extraction at index 0 (N-dim LWE under the TRLWE key)
     uint32_t* o = pool_N + (size_t)it.out * dp.N_stride;
@@ -401,9 +519,6 @@ constexpr int kKsJUnroll = KS_JUNROLL;  // digit-position loop unrolling (icache
 #endif
 #ifndef KS_MINB
 #define KS_MINB 4
-#endif
-#ifndef KS_PAIRS
-#define KS_PAIRS 0
 #endif
 #ifndef KS_CT_DEF
 #define KS_CT_DEF 16
@@ -465,54 +580,6 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
     const size_t row_stride = dp.n_stride;
     const uint4* base = reinterpret_cast<const uint4*>(ksk + col);
     const size_t rs4 = row_stride / 4;
-#if KS_PAIRS
-    // Two digit positions (j, j+1) per step: the 4-bit digit pair of each ciphertext picks
-    // one of 16 cases (warp-uniform: every lane serves the same ciphertext), each a
-    // 3-input add (acc - row_a - row_b) -- half the adds and half the branches.
-    auto sub1 = [](uint4& a, const uint4& r) {
-        a.x -= r.x; a.y -= r.y; a.z -= r.z; a.w -= r.w;
-    };
-    auto sub2 = [](uint4& a, const uint4& r, const uint4& s) {
-        a.x = a.x - r.x - s.x; a.y = a.y - r.y - s.y; a.z = a.z - r.z - s.z; a.w = a.w - r.w - s.w;
-    };
-    for (uint32_t i = 0; i < N; i++) {
-        uint32_t dw[KS_CT / 2];
-        const uint32_t* dp32 = reinterpret_cast<const uint32_t*>(dig + i * KS_CT);
-#pragma unroll
-        for (int c = 0; c < KS_CT / 2; c++)
-            dw[c] = dp32[c];
-#pragma unroll 1
-        for (int jp = 0; jp < 4; jp++) {
-            const uint4* ra = base + ((size_t)i * 24 + (2 * jp) * 3) * rs4;
-            const uint4* rb = ra + 3 * rs4;
-            const uint4 a1 = __ldg(ra), a2 = __ldg(ra + rs4), a3 = __ldg(ra + 2 * rs4);
-            const uint4 b1 = __ldg(rb), b2 = __ldg(rb + rs4), b3 = __ldg(rb + 2 * rs4);
-            const int sh = 12 - 4 * jp;
-#pragma unroll
-            for (int c = 0; c < KS_CT; c++) {
-                const uint32_t w = dw[c >> 1] >> ((c & 1) * 16);
-                switch ((w >> sh) & 15u) {  // (d_j << 2) | d_{j+1}
-                case 1: sub1(acc[c], b1); break;
-                case 2: sub1(acc[c], b2); break;
-                case 3: sub1(acc[c], b3); break;
-                case 4: sub1(acc[c], a1); break;
-                case 5: sub2(acc[c], a1, b1); break;
-                case 6: sub2(acc[c], a1, b2); break;
-                case 7: sub2(acc[c], a1, b3); break;
-                case 8: sub1(acc[c], a2); break;
-                case 9: sub2(acc[c], a2, b1); break;
-                case 10: sub2(acc[c], a2, b2); break;
-                case 11: sub2(acc[c], a2, b3); break;
-                case 12: sub1(acc[c], a3); break;
-                case 13: sub2(acc[c], a3, b1); break;
-                case 14: sub2(acc[c], a3, b2); break;
-                case 15: sub2(acc[c], a3, b3); break;
-                default: break;
-                }
-            }
-        }
-    }
-#else
 #if KS_PREFETCH
     uint4 n1 = __ldg(base), n2 = __ldg(base + rs4), n3 = __ldg(base + 2 * rs4);
 #endif
@@ -552,7 +619,6 @@ __global__ void __launch_bounds__(KS_THREADS, KS_MINB)
             }
         }
     }
-#endif  // KS_PAIRS
 #pragma unroll
     for (int c = 0; c < KS_CT; c++) {
         if ((uint32_t)c < nct) {
