@@ -155,12 +155,6 @@ constexpr uint32_t MAX_CTX_N = 636;
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4  // ciphertexts resident per SM (255 registers per thread)
 #endif
-#ifndef BK_SPLIT
-#define BK_SPLIT 0       // A/B: BK loads split across the transform (see K1)
-#endif
-#ifndef BK_PREFETCH
-#define BK_PREFETCH 0    // 1: BK rows loaded one transform ahead (round 1; 629 vs 617 ms measured in round 2)
-#endif
 
 __device__ __forceinline__ uint32_t rot_read(const uint32_t* p, uint32_t a, int j)
 {
@@ -193,55 +187,6 @@ __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
     im = __fma_rn(F.y, B.x, im);
     acc.x = re;
     acc.y = im;
-}
-
-// ---- ACC_TMEM (A/B knob): the frequency-domain accumulators live in tensor memory
-// (64 TMEM columns per CTA, each thread its own lane) instead of 64 registers, so that
-// 6 CTAs (12 warps) fit per SM.  tcgen05.ld / .st move 16 words per thread at a time.
-#ifndef ACC_TMEM
-#define ACC_TMEM 0
-#endif
-__device__ __forceinline__ void tmem_ld16x2(uint32_t a0, uint32_t a1, uint32_t (&v)[16],
-                                            uint32_t (&w)[16])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15}, [%16];\n"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15])
-        : "r"(a0));
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15}, [%16];\n"
-        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
-          "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
-          "=r"(w[14]), "=r"(w[15])
-        : "r"(a1));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t addr, const uint32_t (&v)[16])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-        "%13,%14,%15,%16};\n"
-        :
-        : "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
-          "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),
-          "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
-__device__ __forceinline__ double2 unpack2(const uint32_t* v)
-{
-    return make_double2(__hiloint2double((int)v[1], (int)v[0]), __hiloint2double((int)v[3], (int)v[2]));
-}
-__device__ __forceinline__ void pack2(uint32_t* v, double2 d)
-{
-    v[0] = (uint32_t)__double2loint(d.x);
-    v[1] = (uint32_t)__double2hiint(d.x);
-    v[2] = (uint32_t)__double2loint(d.y);
-    v[3] = (uint32_t)__double2hiint(d.y);
 }
 
 // ERR = true (diagnostic instantiation only): also record max |w - rint(w)| over every
@@ -299,18 +244,6 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     }
     const FwdTw tw = load_fwd_tw(tb.fwd, t);
     const double2 twt = tb.tw[t];  // psi^t (untwist factors formed on the fly)
-#if ACC_TMEM
-    __shared__ uint32_t acc_tslot;
-    if (t < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;\n" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&acc_tslot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    const uint32_t tacc = acc_tslot + ((uint32_t)(t & 32) << 16);  // this warp's lane quarter
-#endif
     auto bar = [] {
         lpb_jitter();
         __syncthreads();
@@ -337,16 +270,12 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
         LPB_ASSERT(a < 2048u);
         if (a == 0)
             continue;
-#if ACC_TMEM
-        bool first = true;
-#else
         double2 oA[8], oB[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             oA[q] = make_double2(0.0, 0.0);
             oB[q] = make_double2(0.0, 0.0);
         }
-#endif
         const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
 #pragma unroll
         for (int c = 0; c < 2; c++) {
@@ -359,17 +288,8 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             }
 #pragma unroll 1
             for (int p = 0; p < L; p++) {
-                // prefetch this row's BK slots; the loads land while the transform runs
                 const double2* row = bki + (size_t)(c * L + p) * 2 * FFT_M;
                 double2 BA[8], BB[8];
-#if BK_PREFETCH
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BA[q] = ld_stream(row + q * 64 + t);
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
-#endif
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
 #pragma unroll
@@ -378,91 +298,22 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
                     x[q] = make_double2((double)dlo, (double)dhi);
                 }
-#if BK_SPLIT
-                // split prefetch: BA issued early (BK_SPLIT 1: before the transform,
-                // 2: after the cross-warp exchange), BB after the intra-warp exchange
-#if BK_SPLIT == 1
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BA[q] = ld_stream(row + q * 64 + t);
-#endif
-                fwd_pass0(x);
-                exch_p0_to_p1(x, xbuf[xs], t, bar);
-#if BK_SPLIT == 2
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BA[q] = ld_stream(row + q * 64 + t);
-#endif
-                fwd_pass1(x, tw);
-                exch_p1_to_p2(x, xbuf[2], t, wbar);
-#pragma unroll
-                for (int q = 0; q < 8; q++)
-                    BB[q] = ld_stream(row + FFT_M + q * 64 + t);
-                fwd_pass2(x, tw);
-#else
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
-#endif
                 xs ^= 1;
-#if !BK_PREFETCH && !BK_SPLIT && !ACC_TMEM
+                // BK_i rows for this digit, loaded at MAC time (L2-resident): measured faster
+                // than a register prefetch one transform ahead, which spills
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     BA[q] = ld_stream(row + q * 64 + t);
                     BB[q] = ld_stream(row + FFT_M + q * 64 + t);
                 }
-#endif
-#if ACC_TMEM
-                // MAC into the TMEM accumulators, 4 slots (16 words per output) at a time
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-#if !BK_PREFETCH && !BK_SPLIT
-#pragma unroll
-                    for (int qq = 0; qq < 4; qq++) {
-                        BA[4 * h + qq] = ld_stream(row + (4 * h + qq) * 64 + t);
-                        BB[4 * h + qq] = ld_stream(row + FFT_M + (4 * h + qq) * 64 + t);
-                    }
-#endif
-                    uint32_t va[16], vb[16];
-                    if (!first)
-                        tmem_ld16x2(tacc + 16 * h, tacc + 32 + 16 * h, va, vb);
-#pragma unroll
-                    for (int qq = 0; qq < 4; qq++) {
-                        const int q = 4 * h + qq;
-                        double2 oa = first ? make_double2(0.0, 0.0) : unpack2(va + 4 * qq);
-                        double2 ob = first ? make_double2(0.0, 0.0) : unpack2(vb + 4 * qq);
-                        mac(oa, x[q], BA[q]);
-                        mac(ob, x[q], BB[q]);
-                        pack2(va + 4 * qq, oa);
-                        pack2(vb + 4 * qq, ob);
-                    }
-                    tmem_st16(tacc + 16 * h, va);
-                    tmem_st16(tacc + 32 + 16 * h, vb);
-                }
-                tmem_wait_st();
-                first = false;
-#else
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     mac(oA[q], x[q], BA[q]);
                     mac(oB[q], x[q], BB[q]);
                 }
-#endif
             }
         }
-#if ACC_TMEM
-        double2 oA[8], oB[8];
-        {
-            uint32_t va[16], vb[16];
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                tmem_ld16x2(tacc + 16 * h, tacc + 32 + 16 * h, va, vb);
-#pragma unroll
-                for (int qq = 0; qq < 4; qq++) {
-                    oA[4 * h + qq] = unpack2(va + 4 * qq);
-                    oB[4 * h + qq] = unpack2(vb + 4 * qq);
-                }
-            }
-        }
-#endif
         // both inverse transforms in lockstep: shared barriers, twice the ILP.  Tiles:
         // intra and cross exchanges alias xbuf[2] / xbuf[xs] (a CTA barrier separates them)
         {
@@ -484,13 +335,6 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j + 512] += (uint32_t)__double2ll_rn(wb.y);
         }
     }
-#if ACC_TMEM
-    asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (t < 32)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;\n" ::"r"(acc_tslot));
-#endif
     __syncthreads();
     // ---- sample extraction at index 0 (N-dim LWE under the TRLWE key)
     uint32_t* o = pool_N + (size_t)it.out * dp.N_stride;
