@@ -390,6 +390,8 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
     out = {}
     ctx80 = keys80 = None
     for name, (sec, Qfull, R, l, m, enc) in W.CONFIGS.items():
+        if args.locpir_configs and name not in args.locpir_configs.split(","):
+            continue
         if sec == 80:
             if ctx80 is None:
                 p80 = TfheParams(80)
@@ -399,7 +401,8 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
             ctx, keys = ctx80, keys80
         else:
             ctx, keys = ctx128, keys128
-        be = GpuBackend(ctx, keys, torch.device("cuda", local))
+        be = GpuBackend(ctx, keys, torch.device("cuda", local),
+                        staging="host" if BACKEND == "gloo" else "device")
         # flagged modes (not the reference count): "folded" = plaintext-boundary constant
         # folding (plaintext boundaries only), "maj" = majority-borrow
         # comparators (any boundaries)
@@ -496,7 +499,8 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                 "roofline": locpir_roofline(sec, units / Qb, qtot / (ms / 1e3), ws, fp64_peak),
             }
             run.close()
-    out["cfg4_server"] = run_server_sample(ctx128, keys128, ws, max_over_ranks)
+    if not args.locpir_configs or "cfg4" in args.locpir_configs.split(","):
+        out["cfg4_server"] = run_server_sample(ctx128, keys128, ws, max_over_ranks)
     if ctx80 is not None:  # cfg1's latency roof (single query, 80-bit)
         for key in ("cfg1", "cfg1_tree"):
             if key in out:
@@ -665,13 +669,23 @@ def run_server_sample(ctx, keys, ws, max_over_ranks, Q=256, sessions=8):
 
 
 # ---------------------------------------------------------------------------
+# LOCPIR_BENCH_BACKEND=gloo (tests only): N ranks sharing fewer GPUs exchange through host
+# memory; the timing is then not a multi-GPU measurement, the code path is the N > 1 one
+BACKEND = os.environ.get("LOCPIR_BENCH_BACKEND", "nccl")
+
+
 def run_b200(args):
     import torch
     ws, rank, local = dist_env()
+    if BACKEND == "gloo":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2407_19871_b200 import ClientKeys, Context, TfheParams, _abi
 
     params = TfheParams(SECURITY)
@@ -684,9 +698,13 @@ def run_b200(args):
     # ---- keys: generated once (client side) and broadcast over NVLink to every GPU
     from paper_2407_19871_b200.dist import broadcast_keys, max_over_ranks as _mor
     t_setup = time.perf_counter()
-    keys, bk_t, ksk_t = broadcast_keys(params, KEY_SEED, rank, device="cuda")
+    keys, bk_t, ksk_t = broadcast_keys(params, KEY_SEED, rank,
+                                       device=None if BACKEND == "gloo" else "cuda")
     torch.cuda.synchronize()
-    ctx.upload_keys(bk_t.data_ptr(), ksk_t.data_ptr(), on_device=True)
+    if BACKEND == "gloo":
+        ctx.upload_keys(bk_t.numpy().view(np.uint32), ksk_t.numpy().view(np.uint32))
+    else:
+        ctx.upload_keys(bk_t.data_ptr(), ksk_t.data_ptr(), on_device=True)
     del bk_t, ksk_t
 
     # ---- this rank's shard of seeded inputs (client-side encryption)
@@ -707,7 +725,7 @@ def run_b200(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        return _mor(x, device="cuda")
+        return _mor(x, device=None if BACKEND == "gloo" else "cuda")
 
     # ---- device-resident throughput (value)
     for _ in range(args.warmup):
@@ -908,6 +926,8 @@ def main():
                          "sample: LOCPIR_SAMPLES queries per GPU (quick runs)")
     ap.add_argument("--gates", type=int, default=GATES_PER_GPU,
                     help="gates per GPU (default: the cfg2 size; smaller only for profiling)")
+    ap.add_argument("--locpir-configs", default="",
+                    help="comma-separated subset of cfg1,cfg3,cfg4,cfg5 (default: all)")
     ap.add_argument("--emulate-shards", action="store_true",
                     help="also run the N = 2/4/8 LocPIR shards one after another on this GPU")
     ap.add_argument("--dry-run", action="store_true",

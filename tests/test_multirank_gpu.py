@@ -86,3 +86,26 @@ def test_sharded_locpir_world2_on_gpu(tmp_path, mode, staging, sec, Q, R):
                        nprocs=2, join=True, start_method="spawn")
     res = open(tmp_path / "res.txt").read().split()
     assert res == ["1", "1"], res
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu():
+    """The bench's N > 1 code path end to end on real ciphertexts: `bench.py --gpus 2`
+    spawns two ranks (here both on the one leased GPU, exchanging over gloo through host
+    memory: LOCPIR_BENCH_BACKEND=gloo), broadcasts the keys from rank 0, shards the cfg2
+    gates (weak) and the cfg4 queries (gathered to rank 0), takes the max over ranks and
+    prints one line with n_gpus = 2.  The timing of two ranks sharing a GPU is not a
+    multi-GPU number; the correctness of every sharded result is checked."""
+    env = dict(os.environ, LOCPIR_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--gates", "296", "--steps", "2", "--warmup", "1", "--no-cpu-baseline",
+                        "--locpir", "sample", "--locpir-configs", "cfg1,cfg4"],
+                       capture_output=True, text=True, timeout=1500, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["correct"] and d["value"] > 0
+    assert d["locpir"]["cfg4"]["correct"] and d["locpir"]["cfg1"]["correct"]
+    assert d["locpir"]["cfg4"]["queries_per_batch"] == 512  # 256 per rank, gathered
+    assert d["locpir"]["cfg4_server"]["correct"]
