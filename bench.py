@@ -84,26 +84,42 @@ def hbm_view(G, params, avg_br_ms):
 
 
 def keyswitch_view(G, params, avg_ks_ms, ksk_bytes):
-    """K2 (KSK stream) against the INT32 and HBM roofs.  Algorithmic work: N*t digit rows per
-    ciphertext, 3/4 of them non-zero on uniform inputs, n+1 u32 subtractions each.  INT32 peak
-    = 128 lanes/SM x SMs x the clock (nominal B200: unified FP32/INT32 cores)."""
+    """K2t (ks_tc.cuh) against the INT8 tensor-core roof.  The key switch of a level of G
+    ciphertexts is S = A x B with A the (G x K) one-hot digit matrix (K = N t 4) and B the
+    byte-sliced KSK (K x 4(n+1) byte-columns): the MMA issues 2 M_pad K N_pad int8 ops
+    (M padded to 256-row CTAs, N to 256-column tiles).  Peak = 2 x the measured dense bf16
+    rate (MEASURED_PEAKS.json; sm_100's kind::i8 runs at twice kind::f16).  The INT32 view
+    restates the same launch as the 3/4 x N t (n+1) u32 subtractions the CUDA-core K2 does."""
     secs = avg_ks_ms * 1e-3
+    K = params.N * params.c.ks_t * 4
+    m_pad = -(-G // 256) * 256
+    n_stride = -(-(params.n + 1) // 4) * 4
+    n_tiles = -(-(n_stride * 4) // 256)
+    ops = 2.0 * m_pad * K * n_tiles * 256
+    l2_bytes = (m_pad // 256) * n_tiles * K * 256  # every CTA streams its tile's K x 256 bytes
     adds = G * params.N * params.c.ks_t * (params.n + 1) * 0.75
     int_peak = 148 * 128 * 1.965e9
-    dram = committed_traffic("k_keyswitch") if G == GATES_PER_GPU else None
     try:
-        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        i8_peak, hbm_peak = 2 * peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"]
+        src = "2 x MEASURED_PEAKS.json bf16_tflops (burst)"
     except Exception:
-        hbm_peak = None
-    return {"avg_launch_ms": avg_ks_ms,
-            "int32_view": {"achieved_Tops": adds / secs / 1e12, "peak_Tops": int_peak / 1e12,
-                           "frac": adds / secs / int_peak,
-                           "peak_source": "nominal: 148 SMs x 128 INT32 lanes x 1965 MHz"},
+        i8_peak, hbm_peak, src = 4.5e15, None, "nominal B200 dense int8 (no MEASURED_PEAKS.json)"
+    dram = committed_traffic("k_keyswitch_tc") if G == GATES_PER_GPU else None
+    return {"kernel": "k_keyswitch_tc (K2t, tcgen05.mma kind::i8, TMEM accumulators)",
+            "avg_launch_ms": avg_ks_ms,
+            "tensor_view": {"bound": "tensor", "achieved_Tops": ops / secs / 1e12,
+                            "peak_Tops": i8_peak / 1e12, "frac": ops / secs / i8_peak,
+                            "ops_per_launch": ops, "peak_source": src},
+            "int32_equivalent": {"adds_Tops": adds / secs / 1e12,
+                                 "cuda_core_peak_Tops": int_peak / 1e12,
+                                 "note": "the subtractions K2 would do on INT32 lanes "
+                                         "(148 SMs x 128 lanes x 1965 MHz)"},
+            "l2_view": {"l2_to_smem_bytes_per_launch": l2_bytes,
+                        "GBps": l2_bytes / secs / 1e9},
             "hbm_view": {"ksk_bytes": ksk_bytes, "dram_bytes_per_launch": dram,
                          "dram_GBps": dram / secs / 1e9 if dram else None, "peak_GBps": hbm_peak,
-                         "note": "KSK (62 MB) L2-resident; each CTA of 16 ciphertexts re-reads it "
-                                 "from L2 (254 GB/launch of L2->SM traffic at cfg2)"},
-            "ksk_GBps_if_read_once": ksk_bytes / secs / 1e9}
+                         "note": "the tiled KSK (84 MB) stays L2-resident (evict_last bulk copies)"}}
 
 
 def workload_config(n_gpus):

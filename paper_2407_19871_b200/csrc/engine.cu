@@ -19,6 +19,7 @@
 #include "server.hpp"
 #include "circuits.hpp"
 #include "kernels.cuh"
+#include "ks_tc.cuh"
 #include "program.hpp"
 
 using namespace lpb;
@@ -104,6 +105,9 @@ struct locpir_b200_ctx {
     std::string err;
     DevBuf<double2> ftw, itw, TW, bkf;  // per-thread twiddles [8][64] x2, twist [512]
     DevBuf<uint32_t> ksk;
+    DevBuf<uint4> kskt;      // KSK in the tiled byte layout of K2t (ks_tc.cuh)
+    uint32_t kskt_tiles = 0; // N tiles of 256 byte-columns
+    int ks_tc = 1;           // env LOCPIR_B200_KSTC=0: batched levels use K2 instead of K2t
     bool have_keys = false;
     DevBuf<uint32_t> pool_n, pool_N;
     uint64_t pool_slots = 0, scratch_slots = 0;
@@ -405,6 +409,14 @@ void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
         timed_end(c, 1);
         return;
     }
+    if (c->ks_tc && c->kskt_tiles && count >= KT_MIN_COUNT) {
+        k_keyswitch_tc<<<dim3((count + KT_M * KT_HALVES - 1) / (KT_M * KT_HALVES), c->kskt_tiles),
+                         KT_THREADS, KT_SMEM, c->stream>>>(dparams(c), items, count, c->pool_N.p,
+                                                           c->pool_n.p, c->kskt.p);
+        CK(cudaGetLastError());
+        timed_end(c, 1);
+        return;
+    }
     const size_t smem = (size_t)KS_CT * c->p.N * sizeof(uint16_t);
     k_keyswitch<<<blocks, KS_THREADS, smem, c->stream>>>(dparams(c), items, count, c->pool_N.p,
                                                          c->pool_n.p, c->ksk.p);
@@ -531,7 +543,7 @@ void program_enqueue(locpir_b200_ctx* c, const locpir_b200_program* pr, const Br
 // Every device pointer a captured launch sequence bakes in.
 std::vector<const void*> graph_signature(const locpir_b200_ctx* c)
 {
-    return {c->pool_n.p, c->pool_N.p, c->ks_partial.p, c->bkf.p, c->ksk.p,
+    return {c->pool_n.p, c->pool_N.p, c->ks_partial.p, c->bkf.p, c->ksk.p, c->kskt.p,
             c->ftw.p,    c->itw.p,    c->TW.p,         (const void*)c->stream};
 }
 
@@ -656,6 +668,10 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
         CK(cudaMemcpyToSymbol(c_inv4, &T.inv4, sizeof(T.inv4)));
         CK(cudaFuncSetAttribute(k_keyswitch, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(KS_CT * p->N * sizeof(uint16_t))));
+        CK(cudaFuncSetAttribute(k_keyswitch_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)KT_SMEM));
+        if (const char* kt = getenv("LOCPIR_B200_KSTC"))
+            c->ks_tc = strcmp(kt, "0") != 0;
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<3, 7>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLatSmemBytes<3>));
         CK(cudaFuncSetAttribute(k_blind_rotate_lat<2, 10>,
@@ -735,6 +751,15 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
                              (size_t)(c->p.n + 1) * 4, rows_ks,
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              c->stream));
+        // K2t: the KSK as byte-sliced tiles for the INT8 tensor-core key switch
+        if (c->p.N * c->p.ks_t * 4 % KT_KC == 0 && c->p.ks_basebit == 2) {
+            c->kskt_tiles = (c->dp.n_stride * 4 + KT_N - 1) / KT_N;
+            const size_t chunks = (size_t)c->kskt_tiles * (c->p.N * c->p.ks_t * 4 / KT_KC) * 8 * KT_N;
+            c->kskt.reserve(chunks, c->stream, false);
+            k_ksk_to_tc<<<c->num_sms * 16, 256, 0, c->stream>>>(dparams(c), c->ksk.p, c->kskt_tiles,
+                                                                c->kskt.p);
+            CK(cudaGetLastError());
+        }
         CK(cudaStreamSynchronize(c->stream));
         c->have_keys = true;
         // Keep the frequency-domain BK resident in L2 (persisting access window, attached

@@ -322,6 +322,39 @@ def test_pre_keyswitch_coefficients_equal_exact_oracle(dev, level, count, okeys8
         assert np.array_equal(got[g], ok.blind_rotate_extract(lwe[g], mode=oracle.FFT)), g
 
 
+@pytest.mark.parametrize("level", [80, 128])
+@pytest.mark.parametrize("count", [1023, 1024, 4097])
+def test_tensor_core_keyswitch_matches_k2_and_oracle(dev, level, count, okeys80, okeys128,
+                                                     monkeypatch):
+    """K2t (ks_tc.cuh: the key switch as an INT8 tcgen05 contraction, levels of >= 1024
+    ciphertexts) is bit-exact with K2 (a context created with LOCPIR_B200_KSTC=0) on EVERY
+    row and with the oracle on sampled rows.  1023 stays on K2, 1024 is the first K2t
+    level, 4097 leaves a ragged last M tile.  Rows 0..3 pin the digit extremes: all
+    digits 0, all digits 3 (the largest byte sums the int32 accumulators see), and the
+    rounding boundary 2^15 - 1 / 2^15 of the digit decomposition."""
+    from paper_2407_19871_b200 import Context
+    p, keys, ctx = dev[level]
+    ok = okeys80 if level == 80 else okeys128
+    rng = np.random.default_rng(level * 7 + count)
+    lweN = rng.integers(0, 2 ** 32, (count, p.N + 1), dtype=np.uint64).astype(np.uint32)
+    lweN[0, :p.N] = 0
+    lweN[1, :p.N] = 0xFFFF0000
+    lweN[2, :p.N] = 0x7FFF
+    lweN[3, :p.N] = 0x8000
+    got = ctx.debug_keyswitch(lweN)
+    monkeypatch.setenv("LOCPIR_B200_KSTC", "0")
+    k2 = Context(p, 0)
+    try:
+        k2.upload_keys(keys.bk, keys.ksk)
+        want = k2.debug_keyswitch(lweN)
+    finally:
+        k2.close()
+    assert np.array_equal(got, want)
+    idx = sorted(set(range(4)) | set(np.linspace(0, count - 1, 24).astype(int).tolist()))
+    for g in idx:
+        assert np.array_equal(got[g], ok.keyswitch(lweN[g])), g
+
+
 @pytest.mark.parametrize("count", [5, 3000])  # split (small-level) and batched key switch
 def test_keyswitch_bit_exact_on_identical_inputs(dev, count, okeys128):
     """K2 bit-exact against the oracle on identical N-dim inputs."""

@@ -13,11 +13,11 @@ timeout 600 $B > gpurun_out/e_plain.json 2>&1 && \
 B1="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-locpir"
 # steady state: skip the warm-up launches (the first one streams the BK into L2 cold)
 timeout 1500 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sector_hit_rate.pct \
-  --clock-control none -k regex:"^k_blind_rotate$|^k_keyswitch$" --launch-skip 2 -c 2 --csv --log-file gpurun_out/e_traffic.csv $B1 > gpurun_out/e_ncu_traffic.log 2>&1; echo traffic=$? >> gpurun_out/e_status.txt
+  --clock-control none -k regex:"^k_blind_rotate$|^k_keyswitch_tc$" --launch-skip 2 -c 2 --csv --log-file gpurun_out/e_traffic.csv $B1 > gpurun_out/e_ncu_traffic.log 2>&1; echo traffic=$? >> gpurun_out/e_status.txt
 S="python bench.py --gates 4736 --steps 1 --warmup 1 --no-cpu-baseline --no-locpir"
 timeout 300 $S > gpurun_out/e_plain_small.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_blind_rotate$" -c 1 \
   -o gpurun_out/e_prof_br $S > gpurun_out/e_ncu_br.log 2>&1; echo br=$? >> gpurun_out/e_status.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_keyswitch$" -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_keyswitch_tc$" -c 1 \
   -o gpurun_out/e_prof_ks $S > gpurun_out/e_ncu_ks.log 2>&1; echo ks=$? >> gpurun_out/e_status.txt
 cat gpurun_out/e_status.txt

@@ -1,6 +1,6 @@
 """Copy a tools/round_evidence.sh run (gpurun_out/e_*) into the committed profiles/ files:
 bench lines, reference arm, ncu launch list, DRAM traffic per launch, GPU test log, and
-ncu summaries (metrics + top source lines) of K1 and K2."""
+ncu summaries (metrics + top source lines) of K1 and K2t."""
 import csv
 import json
 import os
@@ -32,18 +32,18 @@ def main():
             continue
         if hdr and len(r) == len(hdr):
             x = dict(zip(hdr, r))
-            key = "k_blind_rotate<3, 7>" if "blind_rotate" in x["Kernel Name"] else "k_keyswitch"
+            key = "k_blind_rotate<3, 7>" if "blind_rotate" in x["Kernel Name"] else "k_keyswitch_tc"
             ks.setdefault(key, {})[x["Metric Name"]] = float(x["Metric Value"].replace(",", ""))
     t = {"what": "DRAM bytes read + written and L2 hit rate per launch, steady state (the first "
                  "two launches skipped), cfg2 full size (65,536 gates)",
          "command": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
                     "gpu__time_duration.sum,lts__t_sector_hit_rate.pct --clock-control none "
-                    "-k regex:'^k_blind_rotate$|^k_keyswitch$' --launch-skip 2 -c 2 python "
+                    "-k regex:'^k_blind_rotate$|^k_keyswitch_tc$' --launch-skip 2 -c 2 python "
                     "bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-locpir",
          "kernels": ks}
     json.dump(t, open(os.path.join(P, f"{TAG}_traffic.json"), "w"), indent=1)
     for rep, out, title in (("e_prof_br", f"{TAG}_ncu_blind_rotate.txt", "^k_blind_rotate$"),
-                            ("e_prof_ks", f"{TAG}_ncu_keyswitch.txt", "^k_keyswitch$")):
+                            ("e_prof_ks", f"{TAG}_ncu_keyswitch.txt", "^k_keyswitch_tc$")):
         r = os.path.join(G, rep + ".ncu-rep")
         summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), r],
                               capture_output=True, text=True).stdout
