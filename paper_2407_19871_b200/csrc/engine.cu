@@ -410,7 +410,7 @@ void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
         return;
     }
     if (c->ks_tc && c->kskt_tiles && count >= KT_MIN_COUNT) {
-        k_keyswitch_tc<<<dim3((count + KT_M * KT_HALVES - 1) / (KT_M * KT_HALVES), c->kskt_tiles),
+        k_keyswitch_tc<<<dim3(c->kskt_tiles, (count + KT_M * KT_HALVES - 1) / (KT_M * KT_HALVES)),
                          KT_THREADS, KT_SMEM, c->stream>>>(dparams(c), items, count, c->pool_N.p,
                                                            c->pool_n.p, c->kskt.p);
         CK(cudaGetLastError());
@@ -752,7 +752,7 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              c->stream));
         // K2t: the KSK as byte-sliced tiles for the INT8 tensor-core key switch
-        if (c->p.N * c->p.ks_t * 4 % KT_KC == 0 && c->p.ks_basebit == 2) {
+        if (c->p.N * c->p.ks_t * 4 % (2 * KT_KC) == 0 && c->p.ks_basebit == 2) {  // stage pairs
             c->kskt_tiles = (c->dp.n_stride * 4 + KT_N - 1) / KT_N;
             const size_t chunks = (size_t)c->kskt_tiles * (c->p.N * c->p.ks_t * 4 / KT_KC) * 8 * KT_N;
             c->kskt.reserve(chunks, c->stream, false);

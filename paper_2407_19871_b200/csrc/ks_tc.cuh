@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     __shared__ uint32_t tmem_base_sh;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t nt = blockIdx.y;
-    const uint32_t ct0 = blockIdx.x * (KT_M * KT_HALVES);
+    const uint32_t nt = blockIdx.x;  // adjacent CTAs share one M tile's inputs (L2 hits)
+    const uint32_t ct0 = blockIdx.y * (KT_M * KT_HALVES);
     const uint32_t kc_count = dp.N * dp.t * 4 / KT_KC;
     const uint32_t prec = 1u << (32 - (1 + dp.basebit * dp.t));
 
@@ -249,44 +249,66 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                 a1p[h] = it.in1 != SLOT_NONE ? pool_N + (size_t)it.in1 * dp.N_stride : nullptr;
             }
         }
-        for (uint32_t kc = 0; kc < kc_count; kc++) {
-            const int s = kc % KT_STAGES;
-            if (kc >= KT_STAGES)
-                kt_mbar_wait(&empty_bar[s], ((kc / KT_STAGES) & 1u) ^ 1u);
-            // this stage covers coefficients i = 4 kc .. 4 kc + 3 (t = 8 positions each)
+        // digit words for two stages (8 coefficients = one 32-byte sector per input row)
+        // are loaded one stage pair ahead, so the L2 latency overlaps the previous pair
+        uint4 cur[KT_HALVES][2][2], nxt[KT_HALVES][2][2];  // [half][input][stage of pair]
+        auto load_pair = [&](uint32_t kp, uint4 (&d)[KT_HALVES][2][2]) {
 #pragma unroll
-            for (int h = 0; h < KT_HALVES; h++) {
-                uint4 wv = make_uint4(0, 0, 0, 0);
-                if (a0p[h]) {
-                    wv = __ldg(reinterpret_cast<const uint4*>(a0p[h] + 4 * kc));
-                    if (a1p[h]) {
-                        const uint4 w1 = __ldg(reinterpret_cast<const uint4*>(a1p[h] + 4 * kc));
-                        wv.x += w1.x; wv.y += w1.y; wv.z += w1.z; wv.w += w1.w;
+            for (int h = 0; h < KT_HALVES; h++)
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    d[h][0][e] = a0p[h] ? __ldg(reinterpret_cast<const uint4*>(a0p[h] + 8 * kp + 4 * e))
+                                        : make_uint4(0, 0, 0, 0);
+                    d[h][1][e] = a1p[h] ? __ldg(reinterpret_cast<const uint4*>(a1p[h] + 8 * kp + 4 * e))
+                                        : make_uint4(0, 0, 0, 0);
+                }
+        };
+        load_pair(0, cur);
+        for (uint32_t kp = 0; kp < kc_count / 2; kp++) {
+            if (kp + 1 < kc_count / 2)
+                load_pair(kp + 1, nxt);
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+                const uint32_t kc = 2 * kp + e;
+                const int s = kc % KT_STAGES;
+                if (kc >= KT_STAGES)
+                    kt_mbar_wait(&empty_bar[s], ((kc / KT_STAGES) & 1u) ^ 1u);
+                // this stage covers coefficients i = 4 kc .. 4 kc + 3 (t = 8 positions each)
+#pragma unroll
+                for (int h = 0; h < KT_HALVES; h++) {
+                    const uint4 w0 = cur[h][0][e], w1 = cur[h][1][e];
+                    const uint32_t wd[4] = {(w0.x + w1.x + prec) >> 16, (w0.y + w1.y + prec) >> 16,
+                                            (w0.z + w1.z + prec) >> 16, (w0.w + w1.w + prec) >> 16};
+                    uint8_t* dst = stage_a(s, h) + r * 16;
+                    const bool live = a0p[h] != nullptr;
+#pragma unroll
+                    for (int c = 0; c < 8; c++) {
+                        // chunk c: positions 4c .. 4c+3 of this stage = coefficient c / 2,
+                        // digits j = 4 (c & 1) .. +3; byte 4u + d = [digit == d]
+                        const uint32_t w = wd[c >> 1];
+                        uint32_t o[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int j = 4 * (c & 1) + u;
+                            const uint32_t d = (w >> (14 - 2 * j)) & 3u;
+                            o[u] = live ? 1u << (8 * d) : 0u;
+                        }
+                        *reinterpret_cast<uint4*>(dst + c * (KT_M * 16)) =
+                            make_uint4(o[0], o[1], o[2], o[3]);
                     }
                 }
-                const uint32_t wd[4] = {(wv.x + prec) >> 16, (wv.y + prec) >> 16,
-                                        (wv.z + prec) >> 16, (wv.w + prec) >> 16};
-                uint8_t* dst = stage_a(s, h) + r * 16;
-                const bool live = a0p[h] != nullptr;
-#pragma unroll
-                for (int c = 0; c < 8; c++) {
-                    // chunk c: positions 4c .. 4c+3 of this stage = coefficient c / 2,
-                    // digits j = 4 (c & 1) .. +3; byte 4u + d = [digit == d]
-                    const uint32_t w = wd[c >> 1];
-                    uint32_t o[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int j = 4 * (c & 1) + u;
-                        const uint32_t d = (w >> (14 - 2 * j)) & 3u;
-                        o[u] = live ? 1u << (8 * d) : 0u;
-                    }
-                    *reinterpret_cast<uint4*>(dst + c * (KT_M * 16)) = make_uint4(o[0], o[1], o[2], o[3]);
-                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    kt_mbar_arrive(&full_bar[s]);
             }
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0)
-                kt_mbar_arrive(&full_bar[s]);
+#pragma unroll
+            for (int h = 0; h < KT_HALVES; h++)
+#pragma unroll
+                for (int i = 0; i < 2; i++)
+#pragma unroll
+                    for (int e = 0; e < 2; e++)
+                        cur[h][i][e] = nxt[h][i][e];
         }
         // ---- epilogue: TMEM lane quarter (warp & 3) -> rows r; 64 output columns per half
         kt_mbar_wait(&acc_bar, 0);
