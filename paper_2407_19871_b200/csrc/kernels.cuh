@@ -152,12 +152,6 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
 // MAX_N + 1 entries.
 constexpr int MAX_N = 639;
 constexpr uint32_t MAX_CTX_N = 636;
-#ifndef BR_BK_INLINE
-#define BR_BK_INLINE 0  // A/B: consume each BK load right after it (fewer live registers)
-#endif
-#ifndef BR_TW_RELOAD
-#define BR_TW_RELOAD 0  // A/B: forward twiddles reloaded per transform instead of kept live
-#endif
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4  // ciphertexts resident per SM (255 registers per thread)
 #endif
@@ -182,14 +176,6 @@ __device__ __forceinline__ double2 ld_stream(const double2* p)
         "ld.relaxed.gpu.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], pol;\n\t}"
         : "=d"(v.x), "=d"(v.y)
         : "l"(p));
-    return v;
-}
-
-// twiddle reload at use (A/B BR_TW_RELOAD): volatile so it is not hoisted out of the loop
-__device__ __forceinline__ double2 ld_tw(const double2* p)
-{
-    double2 v;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
     return v;
 }
 
@@ -256,9 +242,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             acc[1][j] = idx < 1024u ? mu : 0u - mu;
         }
     }
-#if !BR_TW_RELOAD
     const FwdTw tw = load_fwd_tw(tb.fwd, t);
-#endif
     const double2 twt = tb.tw[t];  // psi^t (untwist factors formed on the fly)
     auto bar = [] {
         lpb_jitter();
@@ -314,28 +298,10 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                     const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
                     x[q] = make_double2((double)dlo, (double)dhi);
                 }
-#if BR_TW_RELOAD
-                FwdTw tw;
-                {
-                    double2* w = &tw.s3;
-#pragma unroll
-                    for (int e = 0; e < 8; e++)
-                        w[e] = ld_tw(tb.fwd + e * 64 + t);
-                }
-#endif
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
                 // BK_i rows for this digit, loaded at MAC time (L2-resident): measured faster
                 // than a register prefetch one transform ahead, which spills
-#if BR_BK_INLINE
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const double2 ba = ld_stream(row + q * 64 + t);
-                    const double2 bb = ld_stream(row + FFT_M + q * 64 + t);
-                    mac(oA[q], x[q], ba);
-                    mac(oB[q], x[q], bb);
-                }
-#else
 #pragma unroll
                 for (int q = 0; q < 8; q++) {
                     BA[q] = ld_stream(row + q * 64 + t);
@@ -346,7 +312,6 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                     mac(oA[q], x[q], BA[q]);
                     mac(oB[q], x[q], BB[q]);
                 }
-#endif
             }
         }
         // both inverse transforms in lockstep: shared barriers, twice the ILP.  Tiles:
