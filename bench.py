@@ -85,13 +85,14 @@ def hbm_view(G, params, avg_br_ms):
 
 def keyswitch_view(G, params, avg_ks_ms, ksk_bytes):
     """K2t (ks_tc.cuh) against the INT8 tensor-core roof.  The key switch of a level of G
-    ciphertexts is S = A x B with A the (G x K) one-hot digit matrix (K = N t 4) and B the
-    byte-sliced KSK (K x 4(n+1) byte-columns): the MMA issues 2 M_pad K N_pad int8 ops
-    (M padded to 256-row CTAs, N to 256-column tiles).  Peak = 2 x the measured dense bf16
+    ciphertexts is S = A x B with A the (G x K) one-hot digit matrix and B the
+    byte-sliced KSK (K x 4(n+1) byte-columns), K = N t 3 (digit values 1..3; d = 0 adds
+    nothing): the MMA issues 2 M_pad K N_pad int8 ops (M padded to 256-row CTAs, N to
+    256-column tiles).  Peak = 2 x the measured dense bf16
     rate (MEASURED_PEAKS.json; sm_100's kind::i8 runs at twice kind::f16).  The INT32 view
     restates the same launch as the 3/4 x N t (n+1) u32 subtractions the CUDA-core K2 does."""
     secs = avg_ks_ms * 1e-3
-    K = params.N * params.c.ks_t * 4
+    K = params.N * params.c.ks_t * 3
     m_pad = -(-G // 256) * 256
     n_stride = -(-(params.n + 1) // 4) * 4
     n_tiles = -(-(n_stride * 4) // 256)
@@ -119,7 +120,7 @@ def keyswitch_view(G, params, avg_ks_ms, ksk_bytes):
                         "GBps": l2_bytes / secs / 1e9},
             "hbm_view": {"ksk_bytes": ksk_bytes, "dram_bytes_per_launch": dram,
                          "dram_GBps": dram / secs / 1e9 if dram else None, "peak_GBps": hbm_peak,
-                         "note": "the tiled KSK (84 MB) stays L2-resident (evict_last bulk copies)"}}
+                         "note": "the tiled KSK (63 MB at 128-bit) is bulk-copied with evict_last"}}
 
 
 def workload_config(n_gpus):

@@ -752,9 +752,10 @@ int locpir_b200_upload_keys(locpir_b200_ctx* c, const uint32_t* bk, const uint32
                              on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                              c->stream));
         // K2t: the KSK as byte-sliced tiles for the INT8 tensor-core key switch
-        if (c->p.N * c->p.ks_t * 4 % (2 * KT_KC) == 0 && c->p.ks_basebit == 2) {  // stage pairs
+        if (c->p.ks_t == 8 && c->p.ks_basebit == 2 && c->p.N * 8 * 3 % (2 * KT_KC) == 0) {  // stage pairs
             c->kskt_tiles = (c->dp.n_stride * 4 + KT_N - 1) / KT_N;
-            const size_t chunks = (size_t)c->kskt_tiles * (c->p.N * c->p.ks_t * 4 / KT_KC) * 8 * KT_N;
+            const size_t chunks =
+                (size_t)c->kskt_tiles * (c->p.N * c->p.ks_t * 3 / KT_KC) * KT_CHUNKS * KT_N;
             c->kskt.reserve(chunks, c->stream, false);
             k_ksk_to_tc<<<c->num_sms * 16, 256, 0, c->stream>>>(dparams(c), c->ksk.p, c->kskt_tiles,
                                                                 c->kskt.p);

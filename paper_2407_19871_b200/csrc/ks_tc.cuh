@@ -5,7 +5,7 @@
 // where d_ij is the j-th 2-bit digit of a'_i + 2^15.  For a batch of ciphertexts this is a
 // matrix product with a 0/1 matrix:
 //   S[ct][col] = sum_{k = (i, j, d)} A[ct][k] * KSK[i][j][d][col],   A[ct][k] = [d_ij(ct) == d]
-// K = N t 4 = 32,768 (a zero row stands for d = 0).  Every KSK word is split into its four
+// over d = 1..3 only (d = 0 adds nothing): K = N t 3 = 24,576, k = 3 (i t + j) + d - 1.  Every KSK word is split into its four
 // bytes (column 4 col + b holds byte b), so both operands are unsigned 8-bit and the MMA
 // runs as tcgen05.mma kind::i8 with int32 accumulators in tensor memory.  Each byte-column
 // sum is at most N t * 255 = 2,088,960 < 2^31, so the accumulation is exact, and the epilogue
@@ -32,12 +32,18 @@ namespace lpb {
 constexpr int KT_M = 128;             // rows (ciphertexts) per M-half
 constexpr int KT_HALVES = 2;          // M-halves per CTA (share B)
 constexpr int KT_N = 256;             // byte-columns per N tile (64 output columns)
-constexpr int KT_KC = 128;            // K per stage (32 positions x 4 digit values)
-constexpr int KT_STAGES = 3;
+constexpr int KT_KC = 96;             // K per stage (32 positions x digit values 1..3)
+constexpr int KT_CHUNKS = KT_KC / 16; // 16-byte K chunks per row per stage
+constexpr int KT_STAGES = 4;
 constexpr int KT_A_BYTES = KT_M * KT_KC;         // 16 KB per half
 constexpr int KT_B_BYTES = KT_N * KT_KC;         // 32 KB
 constexpr int KT_STAGE_BYTES = KT_HALVES * KT_A_BYTES + KT_B_BYTES;  // 64 KB
-constexpr int KT_THREADS = 256;
+#ifndef KT_BUILD_WARPS
+#define KT_BUILD_WARPS 4
+#endif
+constexpr int KT_BUILDERS = KT_BUILD_WARPS;             // A-producer / epilogue warps (4 or 8)
+constexpr int KT_HPT = KT_HALVES * 4 / KT_BUILDERS;     // M-halves per builder thread
+constexpr int KT_THREADS = 128 + 32 * KT_BUILDERS;
 constexpr uint32_t KT_MIN_COUNT = 1024;  // smaller batched levels keep K2
 constexpr size_t KT_SMEM = (size_t)KT_STAGES * KT_STAGE_BYTES + 1024;
 
@@ -132,30 +138,35 @@ __device__ __forceinline__ void kt_tmem_ld64(uint32_t addr, uint32_t (&v)[64])
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// KSK -> the tiled byte layout the MMA consumes, once per upload.  Block (nt, kc) (32 KB,
-// contiguous) = [c < 8][n < 256][16 bytes]: byte b of chunk c of byte-column n is K index
-// k = kc*128 + 16c + b, i.e. position p = k / 4 (i = p / t, j = p % t) and digit d = k % 4;
-// it holds byte (n % 4) of KSK[i][j][d-1][n / 4] (0 for d = 0 or a padding column).
+// K order inside a stage (96 = 3 digit values x 8 digit positions x 4 coefficients), chosen
+// so the A rows are cheap to build: k = 32 (d - 1) + 4 j + s, where digit position j of
+// coefficient i = 4 kc + KT_SLOT_COEF[s] has value d.
+__host__ __device__ constexpr uint32_t kt_slot_coef(uint32_t s) { return (0x3120u >> (4 * s)) & 15u; }
+
+// KSK -> the tiled byte layout the MMA consumes, once per upload.  Block (nt, kc) (24 KB,
+// contiguous) = [c < 6][n < 256][16 bytes]: byte b of chunk c of byte-column n is K index
+// k = 16c + b of stage kc (order above); it holds byte (n % 4) of KSK[i][j][d-1][n / 4]
+// (0 for a padding column).
 __global__ void k_ksk_to_tc(DevParams dp, const uint32_t* __restrict__ ksk, uint32_t n_tiles,
                             uint4* __restrict__ out)
 {
-    const uint32_t kc_count = dp.N * dp.t * 4 / KT_KC;
-    const uint64_t total = (uint64_t)n_tiles * kc_count * 8 * KT_N;  // 16-byte chunks
+    const uint32_t kc_count = dp.N * dp.t * 3 / KT_KC;
+    const uint64_t total = (uint64_t)n_tiles * kc_count * KT_CHUNKS * KT_N;  // 16-byte chunks
     for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
          e += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t nl = (uint32_t)(e % KT_N);
-        const uint32_t c = (uint32_t)((e / KT_N) % 8);
-        const uint64_t blk = e / (KT_N * 8);
+        const uint32_t c = (uint32_t)((e / KT_N) % KT_CHUNKS);
+        const uint64_t blk = e / (KT_N * KT_CHUNKS);
         const uint32_t kc = (uint32_t)(blk % kc_count), nt = (uint32_t)(blk / kc_count);
         const uint32_t n = nt * KT_N + nl, col = n / 4, byte = n % 4;
         uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int b = 0; b < 16; b++) {
-            const uint32_t k = kc * KT_KC + 16 * c + b;
-            const uint32_t p = k / 4, d = k % 4, i = p / dp.t, j = p % dp.t;
+            const uint32_t kk = 16 * c + b, d = kk / 32, j = (kk % 32) / 4;
+            const uint32_t i = 4 * kc + kt_slot_coef(kk % 4);
             uint32_t v = 0;
-            if (d != 0 && col <= dp.n)
-                v = (ksk[((size_t)(i * dp.t + j) * 3 + (d - 1)) * dp.n_stride + col] >> (8 * byte)) & 255u;
+            if (col <= dp.n)
+                v = (ksk[((size_t)(i * dp.t + j) * 3 + d) * dp.n_stride + col] >> (8 * byte)) & 255u;
             w[b / 4] |= v << (8 * (b % 4));
         }
         out[e] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -175,12 +186,12 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nt = blockIdx.x;  // adjacent CTAs share one M tile's inputs (L2 hits)
     const uint32_t ct0 = blockIdx.y * (KT_M * KT_HALVES);
-    const uint32_t kc_count = dp.N * dp.t * 4 / KT_KC;
+    const uint32_t kc_count = dp.N * dp.t * 3 / KT_KC;
     const uint32_t prec = 1u << (32 - (1 + dp.basebit * dp.t));
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < KT_STAGES; s++) {
-            kt_mbar_init(&full_bar[s], 1 + 4);  // B producer (expect_tx) + 4 A-producer warps
+            kt_mbar_init(&full_bar[s], 1 + KT_BUILDERS);  // B producer (expect_tx) + A-producer warps
             kt_mbar_init(&empty_bar[s], 1);     // tcgen05.commit
         }
         kt_mbar_init(&acc_bar, 1);
@@ -245,6 +256,8 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             a0p[h] = a1p[h] = nullptr;
             if (g < count) {
                 const KsItem it = items[g];
+                LPB_ASSERT(it.in0 < dp.scratch_slots && it.out < dp.pool_slots &&
+                           (it.in1 == SLOT_NONE || it.in1 < dp.scratch_slots));
                 a0p[h] = pool_N + (size_t)it.in0 * dp.N_stride;
                 a1p[h] = it.in1 != SLOT_NONE ? pool_N + (size_t)it.in1 * dp.N_stride : nullptr;
             }
@@ -280,22 +293,25 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                     const uint32_t wd[4] = {(w0.x + w1.x + prec) >> 16, (w0.y + w1.y + prec) >> 16,
                                             (w0.z + w1.z + prec) >> 16, (w0.w + w1.w + prec) >> 16};
                     uint8_t* dst = stage_a(s, h) + r * 16;
-                    const bool live = a0p[h] != nullptr;
+                    const uint32_t live = a0p[h] != nullptr ? 0x01010101u : 0u;
+                    // word (d, j): byte s = [digit j of coefficient kt_slot_coef(s) == d]
+                    const uint32_t P = wd[0] | (wd[1] << 16), Q = wd[2] | (wd[3] << 16);
+                    uint32_t wv[24];
 #pragma unroll
-                    for (int c = 0; c < 8; c++) {
-                        // chunk c: positions 4c .. 4c+3 of this stage = coefficient c / 2,
-                        // digits j = 4 (c & 1) .. +3; byte 4u + d = [digit == d]
-                        const uint32_t w = wd[c >> 1];
-                        uint32_t o[4];
+                    for (int j = 0; j < 8; j++) {
+                        // bytes (c0, c2, c1, c3) of digit j
+                        const uint32_t dj = ((P >> (14 - 2 * j)) & 0x00030003u) |
+                                            (((Q >> (14 - 2 * j)) & 0x00030003u) << 8);
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
-                            const int j = 4 * (c & 1) + u;
-                            const uint32_t d = (w >> (14 - 2 * j)) & 3u;
-                            o[u] = live ? 1u << (8 * d) : 0u;
+                        for (int d = 1; d <= 3; d++) {
+                            const uint32_t y = dj ^ (0x01010101u * (uint32_t)d);  // 0 where equal
+                            wv[8 * (d - 1) + j] = ~(y | (y >> 1)) & live;
                         }
-                        *reinterpret_cast<uint4*>(dst + c * (KT_M * 16)) =
-                            make_uint4(o[0], o[1], o[2], o[3]);
                     }
+#pragma unroll
+                    for (int c = 0; c < KT_CHUNKS; c++)
+                        *reinterpret_cast<uint4*>(dst + c * (KT_M * 16)) =
+                            make_uint4(wv[4 * c], wv[4 * c + 1], wv[4 * c + 2], wv[4 * c + 3]);
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();

@@ -1,5 +1,5 @@
 """Deterministic workload over every product kernel (tools/sanitize_run.py's coverage:
-K0, K1 / K1l, K2 / K2s, K3, K4, K5 and client encryption) at one parameter set; prints
+K0, K1 / K1l, K2t / K2 / K2s, K3, K4, K5 and client encryption) at one parameter set; prints
 one line "digest <sha256>" over ALL outputs.  tools/selfcheck.sh runs it with the default
 and the checked library (LPB_CHECKS device asserts + LPB_JITTER barrier jitter), several
 LOCPIR_B200_POISON patterns for fresh pool / scratch / shared memory, and both kernel
@@ -39,6 +39,14 @@ def main():
         out = ctx.gate_batch_host(kind, a, b)
         assert np.array_equal(keys.decrypt_bits(out), fn(A, B))
         h.update(out.tobytes())
+    # a level large enough for the tensor-core key switch K2t (>= 1,024 and above the
+    # split path's cut in both kernel choices)
+    G2 = 1280
+    A2 = rng.integers(0, 2, G2).astype(np.uint8)
+    B2 = rng.integers(0, 2, G2).astype(np.uint8)
+    out = ctx.gate_batch_host(_abi.NAND, keys.encrypt_bits(A2, 4), keys.encrypt_bits(B2, 5))
+    assert np.array_equal(keys.decrypt_bits(out), 1 - (A2 & B2))
+    h.update(out.tobytes())
     # a small loc_pir batch (comparator chains, masks, XOR tree; K1l/K2s levels and K3)
     bt = W.make_batch(3, 4, 8, 3, seed=5)
     bt.x[0] = (bt.boxes[0, 0] + bt.boxes[0, 1]) // 2
