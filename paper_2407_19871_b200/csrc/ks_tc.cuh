@@ -13,13 +13,13 @@
 // to the subtraction chain of K2 / the oracle (integer sums mod 2^32 are order-free).
 //
 // CTA = 2 x 128 ciphertexts (two M-halves sharing every B tile) x one N tile of 256
-// byte-columns (64 output columns); 256 threads:
+// byte-columns (64 output columns); 384 threads:
 //   warp 0       B producer: one bulk async copy per stage of the pre-tiled KSK block
-//   warp 1       MMA issuer (one thread): 2 halves x 4 K-steps of M128 N256 K32 per stage
+//   warp 1       MMA issuer (one thread): 2 halves x 3 K-steps of M128 N256 K32 per stage
 //   warp 2       TMEM allocator (512 columns: two 128 x 256 int32 accumulators)
-//   warps 4..7   A producers (thread = ciphertext row: one-hot bytes built from the digit
-//                words, stored in the core-matrix layout), then the epilogue (TMEM -> combine
-//                -> pool).  Warp 4 + q reads TMEM lane quarter q.
+//   warps 4..11  A producers (thread = one ciphertext row of one half: one-hot bytes built
+//                from the digit words, stored in the core-matrix layout), then the epilogue
+//                (TMEM -> combine -> pool).  Warp w reads TMEM lane quarter w % 4.
 // Operand layout in shared memory (K-major, SWIZZLE_NONE "interleaved" canonical form):
 // a 16-byte K-chunk c of row r sits at c * LBO + r * 16, so eight consecutive rows form a
 // contiguous 128-byte core matrix (SBO = 128).
@@ -35,13 +35,10 @@ constexpr int KT_N = 256;             // byte-columns per N tile (64 output colu
 constexpr int KT_KC = 96;             // K per stage (32 positions x digit values 1..3)
 constexpr int KT_CHUNKS = KT_KC / 16; // 16-byte K chunks per row per stage
 constexpr int KT_STAGES = 4;
-constexpr int KT_A_BYTES = KT_M * KT_KC;         // 16 KB per half
-constexpr int KT_B_BYTES = KT_N * KT_KC;         // 32 KB
-constexpr int KT_STAGE_BYTES = KT_HALVES * KT_A_BYTES + KT_B_BYTES;  // 64 KB
-#ifndef KT_BUILD_WARPS
-#define KT_BUILD_WARPS 4
-#endif
-constexpr int KT_BUILDERS = KT_BUILD_WARPS;             // A-producer / epilogue warps (4 or 8)
+constexpr int KT_A_BYTES = KT_M * KT_KC;         // 12 KB per half
+constexpr int KT_B_BYTES = KT_N * KT_KC;         // 24 KB
+constexpr int KT_STAGE_BYTES = KT_HALVES * KT_A_BYTES + KT_B_BYTES;  // 48 KB
+constexpr int KT_BUILDERS = 8;  // A-producer / epilogue warps: one row each (4: 3.65 vs 3.12 ms)
 constexpr int KT_HPT = KT_HALVES * 4 / KT_BUILDERS;     // M-halves per builder thread
 constexpr int KT_THREADS = 128 + 32 * KT_BUILDERS;
 constexpr uint32_t KT_MIN_COUNT = 1024;  // smaller batched levels keep K2
@@ -246,13 +243,15 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
             kt_commit(&acc_bar);  // accumulators complete
         }
     } else if (warp >= 4) {
-        // ---- A producers: thread r builds row r of both halves (ciphertexts ct0 + h*128 + r)
-        const int r = threadIdx.x - 128;
-        const uint32_t* a0p[KT_HALVES];
-        const uint32_t* a1p[KT_HALVES];
+        // ---- A producers: thread r builds row r of M-halves h0 .. h0 + KT_HPT - 1
+        // (ciphertexts ct0 + h*128 + r); warp w reads TMEM lane quarter w % 4 in the epilogue
+        const int r = (warp & 3) * 32 + lane;
+        const int h0 = (warp - 4) / 4 * KT_HPT;
+        const uint32_t* a0p[KT_HPT];
+        const uint32_t* a1p[KT_HPT];
 #pragma unroll
-        for (int h = 0; h < KT_HALVES; h++) {
-            const uint32_t g = ct0 + h * KT_M + r;
+        for (int h = 0; h < KT_HPT; h++) {
+            const uint32_t g = ct0 + (h0 + h) * KT_M + r;
             a0p[h] = a1p[h] = nullptr;
             if (g < count) {
                 const KsItem it = items[g];
@@ -264,10 +263,10 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
         }
         // digit words for two stages (8 coefficients = one 32-byte sector per input row)
         // are loaded one stage pair ahead, so the L2 latency overlaps the previous pair
-        uint4 cur[KT_HALVES][2][2], nxt[KT_HALVES][2][2];  // [half][input][stage of pair]
-        auto load_pair = [&](uint32_t kp, uint4 (&d)[KT_HALVES][2][2]) {
+        uint4 cur[KT_HPT][2][2], nxt[KT_HPT][2][2];  // [half][input][stage of pair]
+        auto load_pair = [&](uint32_t kp, uint4 (&d)[KT_HPT][2][2]) {
 #pragma unroll
-            for (int h = 0; h < KT_HALVES; h++)
+            for (int h = 0; h < KT_HPT; h++)
 #pragma unroll
                 for (int e = 0; e < 2; e++) {
                     d[h][0][e] = a0p[h] ? __ldg(reinterpret_cast<const uint4*>(a0p[h] + 8 * kp + 4 * e))
@@ -288,11 +287,11 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                     kt_mbar_wait(&empty_bar[s], ((kc / KT_STAGES) & 1u) ^ 1u);
                 // this stage covers coefficients i = 4 kc .. 4 kc + 3 (t = 8 positions each)
 #pragma unroll
-                for (int h = 0; h < KT_HALVES; h++) {
+                for (int h = 0; h < KT_HPT; h++) {
                     const uint4 w0 = cur[h][0][e], w1 = cur[h][1][e];
                     const uint32_t wd[4] = {(w0.x + w1.x + prec) >> 16, (w0.y + w1.y + prec) >> 16,
                                             (w0.z + w1.z + prec) >> 16, (w0.w + w1.w + prec) >> 16};
-                    uint8_t* dst = stage_a(s, h) + r * 16;
+                    uint8_t* dst = stage_a(s, h0 + h) + r * 16;
                     const uint32_t live = a0p[h] != nullptr ? 0x01010101u : 0u;
                     // word (d, j): byte s = [digit j of coefficient kt_slot_coef(s) == d]
                     const uint32_t P = wd[0] | (wd[1] << 16), Q = wd[2] | (wd[3] << 16);
@@ -319,7 +318,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
                     kt_mbar_arrive(&full_bar[s]);
             }
 #pragma unroll
-            for (int h = 0; h < KT_HALVES; h++)
+            for (int h = 0; h < KT_HPT; h++)
 #pragma unroll
                 for (int i = 0; i < 2; i++)
 #pragma unroll
@@ -331,7 +330,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t lane_addr = (uint32_t)((warp & 3) * 32) << 16;
 #pragma unroll 1
-        for (int h = 0; h < KT_HALVES; h++) {
+        for (int h = h0; h < h0 + KT_HPT; h++) {
             const uint32_t g = ct0 + h * KT_M + r;
             const bool live = g < count;
             KsItem it{};
