@@ -5,7 +5,8 @@
 // where d_ij is the j-th 2-bit digit of a'_i + 2^15.  For a batch of ciphertexts this is a
 // matrix product with a 0/1 matrix:
 //   S[ct][col] = sum_{k = (i, j, d)} A[ct][k] * KSK[i][j][d][col],   A[ct][k] = [d_ij(ct) == d]
-// over d = 1..3 only (d = 0 adds nothing): K = N t 3 = 24,576, k = 3 (i t + j) + d - 1.  Every KSK word is split into its four
+// over d = 1..3 only (d = 0 adds nothing): K = N t 3 = 24,576 (the order of k inside a
+// stage is given at kt_slot_coef).  Every KSK word is split into its four
 // bytes (column 4 col + b holds byte b), so both operands are unsigned 8-bit and the MMA
 // runs as tcgen05.mma kind::i8 with int32 accumulators in tensor memory.  Each byte-column
 // sum is at most N t * 255 = 2,088,960 < 2^31, so the accumulation is exact, and the epilogue
@@ -41,7 +42,7 @@ constexpr int KT_STAGE_BYTES = KT_HALVES * KT_A_BYTES + KT_B_BYTES;  // 48 KB
 constexpr int KT_BUILDERS = 8;  // A-producer / epilogue warps: one row each (4: 3.65 vs 3.12 ms)
 constexpr int KT_HPT = KT_HALVES * 4 / KT_BUILDERS;     // M-halves per builder thread
 constexpr int KT_THREADS = 128 + 32 * KT_BUILDERS;
-constexpr uint32_t KT_MIN_COUNT = 1024;  // smaller batched levels keep K2
+constexpr uint32_t KT_MIN_COUNT = 1024;  // smaller levels: K2s (split) or K2
 constexpr size_t KT_SMEM = (size_t)KT_STAGES * KT_STAGE_BYTES + 1024;
 
 __device__ __forceinline__ uint32_t kt_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
