@@ -398,6 +398,15 @@ void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
     if (!count)
         return;
     timed_begin(c, 1);
+    if (c->ks_tc && c->kskt_tiles && count >= KT_MIN_COUNT) {
+        // K2t: N tiles fast in the grid, one M tile (256 ciphertexts) per grid row
+        k_keyswitch_tc<<<dim3(c->kskt_tiles, (count + KT_M * KT_HALVES - 1) / (KT_M * KT_HALVES)),
+                         KT_THREADS, KT_SMEM, c->stream>>>(dparams(c), items, count, c->pool_N.p,
+                                                           c->pool_n.p, c->kskt.p);
+        CK(cudaGetLastError());
+        timed_end(c, 1);
+        return;
+    }
     const uint32_t blocks = (count + KS_CT - 1) / KS_CT;
     if (c->small_levels && blocks < (uint32_t)c->num_sms / 2) {
         c->ks_partial.reserve((size_t)count * KS_SPLIT * c->dp.n_stride, c->stream, false);
@@ -405,14 +414,6 @@ void launch_ks(locpir_b200_ctx* c, const KsItem* items, uint32_t count)
             dparams(c), items, c->pool_N.p, c->ksk.p, c->ks_partial.p);
         k_ks_reduce<<<count, KS_THREADS, 0, c->stream>>>(dparams(c), items, c->pool_N.p,
                                                           c->ks_partial.p, c->pool_n.p);
-        CK(cudaGetLastError());
-        timed_end(c, 1);
-        return;
-    }
-    if (c->ks_tc && c->kskt_tiles && count >= KT_MIN_COUNT) {
-        k_keyswitch_tc<<<dim3(c->kskt_tiles, (count + KT_M * KT_HALVES - 1) / (KT_M * KT_HALVES)),
-                         KT_THREADS, KT_SMEM, c->stream>>>(dparams(c), items, count, c->pool_N.p,
-                                                           c->pool_n.p, c->kskt.p);
         CK(cudaGetLastError());
         timed_end(c, 1);
         return;

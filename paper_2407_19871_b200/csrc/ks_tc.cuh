@@ -42,7 +42,10 @@ constexpr int KT_STAGE_BYTES = KT_HALVES * KT_A_BYTES + KT_B_BYTES;  // 48 KB
 constexpr int KT_BUILDERS = 8;  // A-producer / epilogue warps: one row each (4: 3.65 vs 3.12 ms)
 constexpr int KT_HPT = KT_HALVES * 4 / KT_BUILDERS;     // M-halves per builder thread
 constexpr int KT_THREADS = 128 + 32 * KT_BUILDERS;
-constexpr uint32_t KT_MIN_COUNT = 1024;  // smaller levels: K2s (split) or K2
+// K2t's launch time is flat (~0.18 ms, one wave) up to ~3,800 ciphertexts; the split K2s
+// grows linearly (0.10 / 0.13 ms at 128, 0.15 / 0.19 ms at 192, 0.83 ms at 1,024 for
+// 80 / 128-bit; tools/ks_sweep.py): K2t from 192 ciphertexts on.
+constexpr uint32_t KT_MIN_COUNT = 192;
 constexpr size_t KT_SMEM = (size_t)KT_STAGES * KT_STAGE_BYTES + 1024;
 
 __device__ __forceinline__ uint32_t kt_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }

@@ -323,13 +323,14 @@ def test_pre_keyswitch_coefficients_equal_exact_oracle(dev, level, count, okeys8
 
 
 @pytest.mark.parametrize("level", [80, 128])
-@pytest.mark.parametrize("count", [1023, 1024, 4097])
+@pytest.mark.parametrize("count", [191, 192, 1183, 4097])
 def test_tensor_core_keyswitch_matches_k2_and_oracle(dev, level, count, okeys80, okeys128,
                                                      monkeypatch):
-    """K2t (ks_tc.cuh: the key switch as an INT8 tcgen05 contraction, levels of >= 1024
-    ciphertexts) is bit-exact with K2 (a context created with LOCPIR_B200_KSTC=0) on EVERY
-    row and with the oracle on sampled rows.  1023 stays on K2, 1024 is the first K2t
-    level, 4097 leaves a ragged last M tile.  Rows 0..3 pin the digit extremes: all
+    """K2t (ks_tc.cuh: the key switch as an INT8 tcgen05 contraction) is bit-exact with K2
+    (a context created with LOCPIR_B200_KSTC=0) on EVERY row and with the oracle on sampled
+    rows.  K2t takes levels of >= 192 ciphertexts: 191 stays on the split K2s in both
+    contexts, 192 is the first K2t level (against K2s), 1183 / 4097 run against the
+    CUDA-core K2, 4097 leaves a ragged last M tile.  Rows 0..3 pin the digit extremes: all
     digits 0, all digits 3 (the largest byte sums the int32 accumulators see), and the
     rounding boundary 2^15 - 1 / 2^15 of the digit decomposition."""
     from paper_2407_19871_b200 import Context

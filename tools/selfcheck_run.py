@@ -39,8 +39,8 @@ def main():
         out = ctx.gate_batch_host(kind, a, b)
         assert np.array_equal(keys.decrypt_bits(out), fn(A, B))
         h.update(out.tobytes())
-    # a level large enough for the tensor-core key switch K2t (>= 1,024 and above the
-    # split path's cut in both kernel choices)
+    # a level that runs K1 (not K1l) and the tensor-core key switch K2t in both kernel
+    # choices
     G2 = 1280
     A2 = rng.integers(0, 2, G2).astype(np.uint8)
     B2 = rng.integers(0, 2, G2).astype(np.uint8)
