@@ -179,6 +179,28 @@ __device__ __forceinline__ double2 ld_stream(const double2* p)
     return v;
 }
 
+// Integer <-> double conversions on the FP64 pipe instead of the conversion unit (XU):
+// digit_to_double(u) = u - HALF for a field value u < 2^20, exact: the bit pattern 2^52 + u
+// minus (2^52 + HALF).  round_low32<SAFE>(w) = rint(w) mod 2^32 (ties to even, as
+// __double2ll_rn): with |w| < 2^51 the sum w + 1.5 * 2^52 is rounded to an integer and its
+// low word is rint(w) mod 2^32.  The external product bounds |w| by 2l N 2^(Bgbit-1) 2^31
+// (+ the < 1/2 transform error): 2^49.6 at 128-bit, so SAFE; 2^52 at 80-bit, which keeps
+// the conversion instruction.
+__device__ __forceinline__ double digit_to_double(uint32_t u, uint32_t half)
+{
+    return __dsub_rn(__hiloint2double(0x43300000, (int)u), 4503599627370496.0 + (double)half);
+}
+template <bool SAFE>
+__device__ __forceinline__ uint32_t round_low32(double w)
+{
+    if constexpr (SAFE)
+        return (uint32_t)__double2loint(__dadd_rn(w, 6755399441055744.0));
+    else
+        return (uint32_t)__double2ll_rn(w);
+}
+template <int L, int BGBIT>
+constexpr bool kMagicRound = (1ull << (BGBIT - 1)) * (2ull * L) * 1024ull < (1ull << 20);
+
 __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
 {
     double re = __fma_rn(F.x, B.x, acc.x);
@@ -293,11 +315,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
                 const int sh = 32 - (p + 1) * BGBIT;
                 double2 x[8];
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const int dlo = (int)((tmp[q] >> sh) & MASK) - (int)HALF;
-                    const int dhi = (int)((tmp[8 + q] >> sh) & MASK) - (int)HALF;
-                    x[q] = make_double2((double)dlo, (double)dhi);
-                }
+                for (int q = 0; q < 8; q++)
+                    x[q] = make_double2(digit_to_double((tmp[q] >> sh) & MASK, HALF),
+                                        digit_to_double((tmp[8 + q] >> sh) & MASK, HALF));
                 fft_forward(x, tw, xbuf[xs], xbuf[2], t, bar, wbar);
                 xs ^= 1;
                 // BK_i rows for this digit, loaded at MAC time (L2-resident): measured faster
@@ -329,10 +349,11 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
             if constexpr (ERR)
                 emax = fmax(emax, fmax(fmax(fabs(wa.x - rint(wa.x)), fabs(wa.y - rint(wa.y))),
                                        fmax(fabs(wb.x - rint(wb.x)), fabs(wb.y - rint(wb.y)))));
-            acc[0][j] += (uint32_t)__double2ll_rn(wa.x);
-            acc[0][j + 512] += (uint32_t)__double2ll_rn(wa.y);
-            acc[1][j] += (uint32_t)__double2ll_rn(wb.x);
-            acc[1][j + 512] += (uint32_t)__double2ll_rn(wb.y);
+            constexpr bool SAFE = kMagicRound<L, BGBIT>;
+            acc[0][j] += round_low32<SAFE>(wa.x);
+            acc[0][j + 512] += round_low32<SAFE>(wa.y);
+            acc[1][j] += round_low32<SAFE>(wb.x);
+            acc[1][j + 512] += round_low32<SAFE>(wb.y);
         }
     }
     __syncthreads();
@@ -813,9 +834,8 @@ __global__ void __launch_bounds__(128 * L, 1)
                 const int j = t + 64 * q;
                 const uint32_t lo = rot_read(S.acc[c], a, j) - S.acc[c][j] + OFF;
                 const uint32_t hi = rot_read(S.acc[c], a, j + 512) - S.acc[c][j + 512] + OFF;
-                const int dlo = (int)((lo >> sh) & MASK) - (int)HALF;
-                const int dhi = (int)((hi >> sh) & MASK) - (int)HALF;
-                x[q] = make_double2((double)dlo, (double)dhi);
+                x[q] = make_double2(digit_to_double((lo >> sh) & MASK, HALF),
+                                    digit_to_double((hi >> sh) & MASK, HALF));
             }
             fft_forward(x, ftw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
 #pragma unroll
@@ -848,8 +868,8 @@ __global__ void __launch_bounds__(128 * L, 1)
             for (int q = 0; q < 8; q++) {
                 const int j = t + 64 * q;
                 const double2 w = cmul(o[q], untwist(twt, q));
-                S.acc[comp][j] += (uint32_t)__double2ll_rn(w.x);
-                S.acc[comp][j + 512] += (uint32_t)__double2ll_rn(w.y);
+                S.acc[comp][j] += round_low32<kMagicRound<L, BGBIT>>(w.x);
+                S.acc[comp][j + 512] += round_low32<kMagicRound<L, BGBIT>>(w.y);
             }
         }
     }
