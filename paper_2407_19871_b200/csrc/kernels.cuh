@@ -806,25 +806,34 @@ __global__ void __launch_bounds__(128 * L, 1)
     // MAC split over all 2L groups: group g serves output component g / L and the
     // frequency slots q*64 + t with q = g % L + L*k (at most P of them per thread); each
     // slot's chain over the 2L rows keeps the oracle's order, so the result is unchanged.
-    constexpr int P = (8 + L - 1) / L;
+    // L = 2: each thread serves BOTH output components for slots q = g, g + 4, so every
+    // digit-spectrum element is read from shared memory once.  L = 3 (384 threads, at the
+    // register limit): each thread serves output component g / L for q = g % L + L k.
+    constexpr bool BOTH = (L == 2);
+    constexpr int P = BOTH ? 2 : (8 + L - 1) / L;
+    constexpr int NO = BOTH ? 2 : 1;  // output components per thread
     const int mcomp = g / L, msub = g % L;
+    auto slot_q = [&](int k) { return BOTH ? g + 2 * L * k : msub + L * k; };
     for (uint32_t i = 0; i < n; i++) {
         __syncthreads();
         const uint32_t a = S.abar[i];
         if (a == 0)
             continue;
         // this thread's BK values for its MAC slots, in flight during the transform
-        double2 bkv[ROWS][P];
+        double2 bkv[ROWS][NO][P];
         {
-            const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M + (size_t)mcomp * FFT_M;
+            const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
 #pragma unroll
             for (int r = 0; r < ROWS; r++)
 #pragma unroll
-                for (int k = 0; k < P; k++) {
-                    const int q = msub + L * k;
-                    if (q < 8)
-                        bkv[r][k] = ld_stream(bki + (size_t)r * 2 * FFT_M + q * 64 + t);
-                }
+                for (int o = 0; o < NO; o++)
+#pragma unroll
+                    for (int k = 0; k < P; k++) {
+                        const int q = slot_q(k);
+                        const int comp = BOTH ? o : mcomp;
+                        if (q < 8)
+                            bkv[r][o][k] = ld_stream(bki + ((size_t)r * 2 + comp) * FFT_M + q * 64 + t);
+                    }
         }
         // every group: digit (c, p) of (X^a - 1) ACC_c -> forward transform -> F[g]
         {
@@ -845,13 +854,22 @@ __global__ void __launch_bounds__(128 * L, 1)
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < P; k++) {
-            const int q = msub + L * k;
+            const int q = slot_q(k);
             if (q < 8) {
-                double2 o = make_double2(0.0, 0.0);
+                double2 oo[NO];
 #pragma unroll
-                for (int r = 0; r < ROWS; r++)
-                    mac(o, S.F[r][q * 64 + t], bkv[r][k]);
-                S.O[mcomp][q * 64 + t] = o;
+                for (int o = 0; o < NO; o++)
+                    oo[o] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int r = 0; r < ROWS; r++) {
+                    const double2 F = S.F[r][q * 64 + t];
+#pragma unroll
+                    for (int o = 0; o < NO; o++)
+                        mac(oo[o], F, bkv[r][o][k]);
+                }
+#pragma unroll
+                for (int o = 0; o < NO; o++)
+                    S.O[BOTH ? o : mcomp][q * 64 + t] = oo[o];
             }
         }
         __syncthreads();
