@@ -83,6 +83,36 @@ def hbm_view(G, params, avg_br_ms):
             "peak_GBps": peak, "frac": (t or alg) / secs / 1e9 / peak if peak else None}
 
 
+def l1tex_view():
+    """The unit that actually binds K1: L1TEX data-pipe utilisation and the
+    per-CMux-step wavefront budget, from the newest committed ncu --set full capture
+    (profiles/r0N_ncu_blind_rotate.txt); None when absent."""
+    for tag in ("r02", "r01"):
+        try:
+            txt = open(os.path.join(ROOT, "profiles", f"{tag}_ncu_blind_rotate.txt")).read()
+        except OSError:
+            continue
+        m = {}
+        for ln in txt.splitlines():
+            parts = ln.split()
+            if len(parts) == 2 and parts[0].startswith(("l1tex__", "sm__pipe_fp64", "launch__grid")):
+                try:
+                    m[parts[0]] = float(parts[1])
+                except ValueError:
+                    pass
+        util = m.get("l1tex__throughput.avg.pct_of_peak_sustained_active")
+        wf = m.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")
+        grid = m.get("launch__grid_size")
+        return {"l1tex_utilisation": util / 100 if util else None,
+                "fp64_pipe_utilisation": (m.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active") or 0) / 100 or None,
+                "shared_wavefronts_per_cmux_step": wf / (grid * 630) if wf and grid else None,
+                "source": f"profiles/{tag}_ncu_blind_rotate.txt (4,736 ciphertexts, 128-bit)",
+                "note": "peak is one wavefront per clock per SM; the transform exchanges, BK "
+                        "loads and ACC reads keep L1TEX the busiest unit, so 1 - this "
+                        "utilisation bounds what better scheduling alone can recover"}
+    return None
+
+
 def keyswitch_view(G, params, avg_ks_ms, ksk_bytes):
     """K2t (ks_tc.cuh) against the INT8 tensor-core roof.  The key switch of a level of G
     ciphertexts is S = A x B with A the (G x K) one-hot digit matrix and B the
@@ -821,6 +851,7 @@ def run_b200(args):
                               "with no shared contraction (SURVEY §8(d)), so neither the HBM "
                               "nor the tensor-core roof applies; hbm_view shows the HBM side",
                 "hbm_view": hbm_view(G, params, avg_br_ms),
+                "l1tex_view": l1tex_view(),
             },
             "keyswitch": keyswitch_view(G, params, avg_ks_ms, ksk_bytes),
             "e2e": {"value": ws * G / e2e_s, "unit": "gates/s",
