@@ -70,6 +70,27 @@ def test_mux_bit_exact_with_oracle(dev, okeys128):
 
 
 @pytest.mark.parametrize("level", [80, 128])
+def test_wide_mux_level_bit_exact_with_oracle(dev, level, okeys80, okeys128):
+    """A level of 300 MUX gates: the 600 blind rotations run on K1 and the 300 combined key
+    switches (two N-dim inputs summed, + 1/8) on the tensor-core K2t -- its two-input path.
+    Every output decrypts to the MUX truth and 12 sampled rows equal the oracle's gate."""
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[level]
+    ok = okeys80 if level == 80 else okeys128
+    G = 300
+    rng = np.random.default_rng(level + 17)
+    S, X, Y = (rng.integers(0, 2, G).astype(np.uint8) for _ in range(3))
+    s, x, y = keys.encrypt_bits(S, 41), keys.encrypt_bits(X, 42), keys.encrypt_bits(Y, 43)
+    ctx.pool_reserve(4 * G)
+    ctx.h2d(0, np.concatenate([s, x, y]))
+    ctx.run([(_abi.MUX, g, G + g, 2 * G + g, 3 * G + g) for g in range(G)])
+    out = ctx.d2h(3 * G, G)
+    assert np.array_equal(keys.decrypt_bits(out), np.where(S == 1, X, Y))
+    for g in np.linspace(0, G - 1, 12).astype(int):
+        assert np.array_equal(out[g], ok.gate("mux", s[g], x[g], y[g])), g
+
+
+@pytest.mark.parametrize("level", [80, 128])
 def test_truth_tables_many_seeds(dev, level):
     """acceptance.cpp:334-375: every gate, both inputs, many encryption seeds."""
     from paper_2407_19871_b200 import _abi
