@@ -18,6 +18,7 @@ S="python bench.py --gates 4736 --steps 1 --warmup 1 --no-cpu-baseline --no-locp
 timeout 300 $S > gpurun_out/e_plain_small.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_blind_rotate$" -c 1 \
   -o gpurun_out/e_prof_br $S > gpurun_out/e_ncu_br.log 2>&1; echo br=$? >> gpurun_out/e_status.txt
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^k_keyswitch_tc$" -c 1 \
-  -o gpurun_out/e_prof_ks $S > gpurun_out/e_ncu_ks.log 2>&1; echo ks=$? >> gpurun_out/e_status.txt
+# K2t at cfg2 size (at 4,736 gates its grid is only 1.3 waves)
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"^k_keyswitch_tc$" --launch-skip 1 -c 1 \
+  -o gpurun_out/e_prof_ks $B1 > gpurun_out/e_ncu_ks.log 2>&1; echo ks=$? >> gpurun_out/e_status.txt
 cat gpurun_out/e_status.txt

@@ -52,8 +52,10 @@ def main():
         open("/tmp/_src.csv", "w").write(src)
         lines = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), "/tmp/_src.csv"],
                                capture_output=True, text=True).stdout.splitlines()[:26]
+        size = ("--gates 4736 --steps 1 --warmup 1" if rep == "e_prof_br" else
+                "--steps 1 --warmup 1 (cfg2 size, --launch-skip 1)")
         hdr_line = (f"# ncu --set full --clock-control none --import-source on -k regex:'{title}' -c 1 "
-                    f"python bench.py --gates 4736 --steps 1 --warmup 1 --no-cpu-baseline --no-locpir\n")
+                    f"python bench.py {size} --no-cpu-baseline --no-locpir\n")
         open(os.path.join(P, out), "w").write(hdr_line + summ + "\n# top CUDA source lines by warp-stall samples\n"
                                               + "\n".join(lines) + "\n")
     print("profiles updated")
