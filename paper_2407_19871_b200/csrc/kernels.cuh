@@ -200,6 +200,8 @@ __device__ __forceinline__ uint32_t round_low32(double w)
 }
 template <int L, int BGBIT>
 constexpr bool kMagicRound = (1ull << (BGBIT - 1)) * (2ull * L) * 1024ull < (1ull << 20);
+static_assert(kMagicRound<3, 7>, "128-bit: |w| <= 6 * 1024 * 2^6 * 2^31 = 2^49.6 < 2^51");
+static_assert(!kMagicRound<2, 10>, "80-bit: the bound 4 * 1024 * 2^9 * 2^31 = 2^52 is not < 2^51");
 
 __device__ __forceinline__ void mac(double2& acc, double2 F, double2 B)
 {
