@@ -152,6 +152,15 @@ __global__ void __launch_bounds__(64) k_bk_to_freq(const uint32_t* __restrict__ 
 // MAX_N + 1 entries.
 constexpr int MAX_N = 639;
 constexpr uint32_t MAX_CTX_N = 636;
+#ifndef LAT_BK_SPREAD
+#define LAT_BK_SPREAD 1  // K1l: BK loads issued between the forward passes
+#endif
+#ifndef LAT_BK_B0
+#define LAT_BK_B0 2  // rows loaded before pass 0 / before pass 1 (cumulative) / rest before pass 2
+#endif
+#ifndef LAT_BK_B1
+#define LAT_BK_B1 4
+#endif
 #ifndef BR_MIN_BLOCKS
 #define BR_MIN_BLOCKS 4  // ciphertexts resident per SM (255 registers per thread)
 #endif
@@ -816,17 +825,29 @@ __global__ void __launch_bounds__(128 * L, 1)
     constexpr int NO = BOTH ? 2 : 1;  // output components per thread
     const int mcomp = g / L, msub = g % L;
     auto slot_q = [&](int k) { return BOTH ? g + 2 * L * k : msub + L * k; };
+#ifdef LPB_PHASE_CLK
+    // diagnostic build only: per-phase clock sums of thread 0 of CTA 0
+    unsigned long long ph[12] = {0}, tp = clock64();
+    auto mark = [&](int k) {
+        const unsigned long long now = clock64();
+        ph[k] += now - tp;
+        tp = now;
+    };
+#else
+    auto mark = [](int) {};
+#endif
     for (uint32_t i = 0; i < n; i++) {
         __syncthreads();
+        mark(0);
         const uint32_t a = S.abar[i];
         if (a == 0)
             continue;
         // this thread's BK values for its MAC slots, in flight during the transform
         double2 bkv[ROWS][NO][P];
-        {
-            const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
+        const double2* bki = bkf + (size_t)i * ROWS * 2 * FFT_M;
+        auto load_rows = [&](int r0, int r1) {
 #pragma unroll
-            for (int r = 0; r < ROWS; r++)
+            for (int r = r0; r < r1; r++)
 #pragma unroll
                 for (int o = 0; o < NO; o++)
 #pragma unroll
@@ -836,7 +857,16 @@ __global__ void __launch_bounds__(128 * L, 1)
                         if (q < 8)
                             bkv[r][o][k] = ld_stream(bki + ((size_t)r * 2 + comp) * FFT_M + q * 64 + t);
                     }
-        }
+        };
+        // l = 3: the BK loads are issued in thirds AFTER the digit reads and each exchange,
+        // so they drain through L1TEX during the FP64 passes instead of queueing in front
+        // of the rotated ACC reads (K1l launch 2.30 -> 2.23 ms); l = 2: all up front
+        // (spreading them measured 1.27 -> 1.36 ms).  tools/r3_k1l_ab.sh
+        constexpr bool SPREAD = LAT_BK_SPREAD && L == 3;
+        constexpr int B0 = SPREAD ? LAT_BK_B0 : ROWS;
+        constexpr int B1 = SPREAD ? (LAT_BK_B1 < ROWS ? LAT_BK_B1 : ROWS) : ROWS;
+        if constexpr (!SPREAD)
+            load_rows(0, ROWS);
         // every group: digit (c, p) of (X^a - 1) ACC_c -> forward transform -> F[g]
         {
             double2 x[8];
@@ -848,12 +878,30 @@ __global__ void __launch_bounds__(128 * L, 1)
                 x[q] = make_double2(digit_to_double((lo >> sh) & MASK, HALF),
                                     digit_to_double((hi >> sh) & MASK, HALF));
             }
-            fft_forward(x, ftw, S.tiles[g][0], S.tiles[g][1], t, bar, wbar);
+            mark(6);
+            if constexpr (SPREAD)
+                load_rows(0, B0);
+            fwd_pass0(x);
+            mark(7);
+            exch_p0_to_p1(x, S.tiles[g][0], t, bar);
+            mark(8);
+            if constexpr (SPREAD)
+                load_rows(B0, B1);
+            fwd_pass1(x, ftw);
+            mark(9);
+            exch_p1_to_p2(x, S.tiles[g][1], t, wbar);
+            mark(10);
+            if constexpr (SPREAD)
+                load_rows(B1, ROWS);
+            fwd_pass2(x, ftw);
+            mark(11);
 #pragma unroll
             for (int q = 0; q < 8; q++)
                 S.F[g][q * 64 + t] = x[q];
         }
+        mark(1);
         __syncthreads();
+        mark(2);
 #pragma unroll
         for (int k = 0; k < P; k++) {
             const int q = slot_q(k);
@@ -874,7 +922,9 @@ __global__ void __launch_bounds__(128 * L, 1)
                     S.O[BOTH ? o : mcomp][q * 64 + t] = oo[o];
             }
         }
+        mark(3);
         __syncthreads();
+        mark(4);
         // groups 0 / 1: inverse transform of output component g, ACC update
         if (g < 2) {
             const int comp = g;
@@ -892,7 +942,18 @@ __global__ void __launch_bounds__(128 * L, 1)
                 S.acc[comp][j + 512] += round_low32<kMagicRound<L, BGBIT>>(w.y);
             }
         }
+        mark(5);
     }
+#ifdef LPB_PHASE_CLK
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("K1l<%d> phase clocks per step (n=%u): top-barrier %.0f fwd %.0f fwd-barrier %.0f "
+               "mac %.0f mac-barrier %.0f inverse %.0f\n", L, n, ph[0] / (double)n, ph[1] / (double)n,
+               ph[2] / (double)n, ph[3] / (double)n, ph[4] / (double)n, ph[5] / (double)n);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("  fwd split: digits %.0f pass0 %.0f xchg1 %.0f pass1 %.0f xchg2 %.0f pass2 %.0f\n",
+               ph[6] / (double)n, ph[7] / (double)n, ph[8] / (double)n, ph[9] / (double)n,
+               ph[10] / (double)n, ph[11] / (double)n);
+#endif
     __syncthreads();
     uint32_t* out = pool_N + (size_t)it.out * dp.N_stride;
     for (int j = threadIdx.x; j < 1024; j += blockDim.x)
