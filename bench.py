@@ -536,7 +536,7 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                          "reference gate count)") if tree else
                         ("flagged: plaintext boundaries constant-folded (not the reference "
                          "gate count)") if folded else
-                        ("flagged: majority-borrow comparators, N(4l+2m+3) units (not the "
+                        ("flagged: majority-borrow comparators, N(4l+2m+3)-m units (not the "
                          "reference gate count)") if maj else
                         "reference circuit (N(12l+2m+3) units)",
                 "programs": len(run.progs),

@@ -54,6 +54,10 @@ extern "C" {
 #define LOCPIR_B200_ORNY 11  /* OR(NOT in0, in1):  one bootstrap, form (+1/8, -1, +1) */
 #define LOCPIR_B200_MAJ 12   /* MAJ(in0, in1, in2): one bootstrap of in0 + in1 + in2 (three
                                 +-1/8 never sum to 0); counted in bootstrap_units */
+#define LOCPIR_B200_XOR3 13  /* in0 ^ in1 ^ in2: one bootstrap of -2 (in0 + in1 + in2) -- an
+                                odd count of true inputs lands on +1/4, an even count on
+                                -1/4 (mod 1), the margins of the 2-input XOR; flagged
+                                modes' ternary XOR trees; counted in bootstrap_units */
 
 /* Full TFHE parameter set (extends TlweParams {n, sigma}, torus.hpp:71-110). */
 typedef struct locpir_b200_params {
@@ -301,7 +305,9 @@ uint64_t locpir_b200_loc_pir_folded_scratch(uint32_t Q, uint32_t R, uint32_t l, 
 /* Flagged mode: comparators as a majority borrow chain (works with ENCRYPTED boundaries,
  * cfg5): with the sign bits flipped, a < b = borrow out of a - b,
  * borrow_{i+1} = MAJ(NOT a_i, b_i, borrow_i), borrow_0 = 0 -- l bootstraps per comparator
- * instead of 3l, same depth; a region costs 4l + 2m + 3.  Same arguments as
+ * instead of 3l, same depth; a region costs 4l + 2m + 3, minus m per query: like every
+ * flagged mode it skips the bootstrapped XOR with Enc(0) that starts each bit column of
+ * the reference's XOR sum (one circuit level).  Same arguments as
  * locpir_b200_loc_pir_program; decrypted results equal the reference circuit's. */
 int locpir_b200_loc_pir_maj_program(uint32_t Q, uint32_t R, uint32_t l, uint32_t m,
                                     const uint32_t* x_slots, const uint32_t* y_slots,

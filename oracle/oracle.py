@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(HERE, "build", "liboracle.so")
 
 EXACT, FFT = 0, 1
 GATES = {"and": 0, "or": 1, "xor": 2, "xnor": 3, "nand": 4, "mux": 5, "not": 6, "nor": 7,
-         "andny": 10, "orny": 11, "maj": 12}
+         "andny": 10, "orny": 11, "maj": 12, "xor3": 13}
 
 
 class GateItem(C.Structure):

@@ -828,6 +828,11 @@ int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
         for (uint32_t q = 0; q <= n; q++)
             comb[q] += c[q];
         break;
+    case OR_GATE_XOR3:
+        lin2(n, 0u, -2, a, -2, b, comb);
+        for (uint32_t q = 0; q <= n; q++)
+            comb[q] += (uint32_t)-2 * c[q];
+        break;
     case OR_GATE_NOT:
         for (uint32_t q = 0; q <= n; q++)
             out[q] = 0u - a[q];

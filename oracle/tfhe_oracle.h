@@ -150,7 +150,8 @@ enum {
     OR_GATE_NOR = 7,
     OR_GATE_ANDNY = 10, /* AND(NOT a, b): flagged constant-folding mode */
     OR_GATE_ORNY = 11,  /* OR(NOT a, b) */
-    OR_GATE_MAJ = 12    /* MAJ(a, b, c) = BS(a + b + c): flagged majority-comparator mode */
+    OR_GATE_MAJ = 12,   /* MAJ(a, b, c) = BS(a + b + c): flagged majority-comparator mode */
+    OR_GATE_XOR3 = 13   /* a ^ b ^ c = BS(-2 (a + b + c)): flagged ternary XOR trees */
 };
 /* out = gate(a, b[, c]) ; for MUX: out = a ? b : c.  n-dim in/out. */
 int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LOCPIR_B200_LIB") or os.path.join(HERE, "liblocpir_b200.so")
 
 OK, EINVAL, ELOGIC, ECUDA, ENOMEM = 0, -1, -2, -3, -4
-AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST, ANDNY, ORNY, MAJ = range(13)
+AND, OR, XOR, XNOR, NAND, MUX, NOT, NOR, COPY, CONST, ANDNY, ORNY, MAJ, XOR3 = range(14)
 SLOT_NONE = 0xFFFFFFFF
 
 

@@ -160,21 +160,51 @@ inline uint64_t loc_pir_scratch(uint32_t Q, uint32_t R, uint32_t l, uint32_t m)
 // N boxes, as the reference chain).  mode 2 (box-sharded partial): the root
 // is copied to dst without the XOR with Enc(0) (N-1 units); the rank-0 combine adds one
 // XOR per shard plus the one with Enc(0), so the total stays N units.
+// ternary (flagged modes): XOR3 nodes (one bootstrap each), so the tree has ceil(log3 N)
+// levels and about (N - 1) / 2 bootstraps instead of log2 N levels and N - 1.
 inline void emit_xor_root(Emitter& e, std::vector<uint32_t> lvl, uint32_t zero, uint32_t dst,
-                          int mode)
+                          int mode, bool ternary = false)
 {
     while (lvl.size() > 1) {
         std::vector<uint32_t> nxt;
-        for (size_t i = 0; i + 1 < lvl.size(); i += 2)
+        size_t i = 0;
+        if (ternary)
+            for (; i + 2 < lvl.size(); i += 3)
+                nxt.push_back(e.gate(LOCPIR_B200_XOR3, lvl[i], lvl[i + 1], lvl[i + 2]));
+        for (; i + 1 < lvl.size(); i += 2)
             nxt.push_back(e.gate(LOCPIR_B200_XOR, lvl[i], lvl[i + 1]));
-        if (lvl.size() & 1)
+        if (i < lvl.size())
             nxt.push_back(lvl.back());
         lvl.swap(nxt);
     }
-    if (mode == 2)
+    if (mode == 2 || zero == 0xFFFFFFFFu)
         e.gate(LOCPIR_B200_COPY, lvl[0], 0xFFFFFFFFu, 0xFFFFFFFFu, dst);
     else
         e.gate(LOCPIR_B200_XOR, zero, lvl[0], 0xFFFFFFFFu, dst);
+}
+
+// XOR-sum of one bit column into dst.  The reference starts every column from Enc(0)
+// (circuits.hpp:257-261) and bootstraps that XOR too; the flagged modes (already not the
+// reference gate count) skip it -- the XOR with a trivial zero only refreshes a value that
+// is itself a fresh bootstrap output, and it costs a whole circuit level (the last one) --
+// and reduce the column with a ternary XOR3 tree.
+inline void emit_xor_column(Emitter& e, const std::vector<uint32_t>& lvl, uint32_t dst,
+                            int xor_tree, bool flagged)
+{
+    const uint32_t zero = flagged && xor_tree != 2 ? 0xFFFFFFFFu : e.gate(LOCPIR_B200_CONST, 0);
+    if (xor_tree) {
+        emit_xor_root(e, lvl, zero, dst, xor_tree, flagged);
+        return;
+    }
+    const size_t R = lvl.size();
+    uint32_t acc = zero;
+    for (size_t r = 0; r < R; r++) {
+        const uint32_t o = r + 1 == R ? dst : 0xFFFFFFFFu;
+        if (acc == 0xFFFFFFFFu)  // flagged chain: starts from the first term
+            acc = R == 1 ? e.gate(LOCPIR_B200_COPY, lvl[0], 0xFFFFFFFFu, 0xFFFFFFFFu, o) : lvl[0];
+        else
+            acc = e.gate(LOCPIR_B200_XOR, acc, lvl[r], 0xFFFFFFFFu, o);
+    }
 }
 
 // loc_pir (circuits.hpp:276-324) for Q queries.  xor_tree = 0 keeps the
@@ -223,21 +253,12 @@ inline void emit_loc_pir_fn(std::vector<locpir_b200_gate_op>& ops, uint32_t Q, u
             for (uint32_t j = 0; j < m; j++)  // mask_service (circuits.hpp:219-227)
                 masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc(q, r, j));
         }
-        // xor_sum_services (circuits.hpp:240-269)
+        // xor_sum_services (circuits.hpp:240-269); cmp != 0 is a flagged mode
+        std::vector<uint32_t> lvl(R);
         for (uint32_t j = 0; j < m; j++) {
-            const uint32_t dst = out[(size_t)q * m + j];
-            const uint32_t zero = e.gate(LOCPIR_B200_CONST, 0);
-            if (!xor_tree) {
-                uint32_t acc = zero;
-                for (uint32_t r = 0; r < R; r++)
-                    acc = e.gate(LOCPIR_B200_XOR, acc, masked[(size_t)r * m + j], 0xFFFFFFFFu,
-                                 r + 1 == R ? dst : 0xFFFFFFFFu);
-            } else {
-                std::vector<uint32_t> lvl(R);
-                for (uint32_t r = 0; r < R; r++)
-                    lvl[r] = masked[(size_t)r * m + j];
-                emit_xor_root(e, lvl, zero, dst, xor_tree);
-            }
+            for (uint32_t r = 0; r < R; r++)
+                lvl[r] = masked[(size_t)r * m + j];
+            emit_xor_column(e, lvl, out[(size_t)q * m + j], xor_tree, cmp != 0);
         }
     }
 }
@@ -321,19 +342,11 @@ inline void emit_loc_pir_folded_fn(std::vector<locpir_b200_gate_op>& ops, uint32
             for (uint32_t j = 0; j < m; j++)
                 masked[(size_t)r * m + j] = e.gate(LOCPIR_B200_AND, f, svc(q, r, j));
         }
-        for (uint32_t j = 0; j < m; j++) {
-            const uint32_t dst = out[(size_t)q * m + j];
-            const uint32_t zero = e.gate(LOCPIR_B200_CONST, 0);
-            std::vector<uint32_t> lvl(R);
+        std::vector<uint32_t> lvl(R);
+        for (uint32_t j = 0; j < m; j++) {  // flagged mode: no XOR with Enc(0)
             for (uint32_t r = 0; r < R; r++)
                 lvl[r] = masked[(size_t)r * m + j];
-            if (!xor_tree) {
-                uint32_t acc = zero;
-                for (uint32_t r = 0; r < R; r++)
-                    acc = e.gate(LOCPIR_B200_XOR, acc, lvl[r], 0xFFFFFFFFu, r + 1 == R ? dst : 0xFFFFFFFFu);
-                continue;
-            }
-            emit_xor_root(e, lvl, zero, dst, xor_tree);
+            emit_xor_column(e, lvl, out[(size_t)q * m + j], xor_tree, true);
         }
     }
 }

@@ -35,7 +35,7 @@ struct Plan {
     std::vector<std::vector<LinItem>> lin;  // per wave (run before the wave's BR)
     uint32_t scratch = 0;                   // N-dim scratch slots needed
     uint64_t n_br = 0, n_ks = 0;
-    uint64_t counts[10] = {0};              // and or xor xnor not mux nand nor units maj
+    uint64_t counts[10] = {0};              // and or xor xnor not mux nand nor units, [9] flagged 3-input gates (MAJ, XOR3)
     uint32_t waves() const { return (uint32_t)br.size(); }
 };
 
@@ -160,15 +160,17 @@ inline Plan build_plan(const locpir_b200_gate_op* ops, uint64_t count)
             // counters: ANDNY / ORNY count as AND / OR
             static const int cidx[] = {0, 1, 2, 3, 6, -1, -1, 7, -1, -1, 0, 1};
             P.counts[cidx[op.kind]]++;
-        } else if (op.kind == LOCPIR_B200_MAJ) {
-            // 3-input majority: BS(in0 + in1 + in2) -- the sum of three +-1/8 never hits 0
+        } else if (op.kind == LOCPIR_B200_MAJ || op.kind == LOCPIR_B200_XOR3) {
+            // 3-input majority: BS(in0 + in1 + in2) -- the sum of three +-1/8 never hits 0;
+            // 3-input XOR: BS(-2 (in0 + in1 + in2)) -- +1/4 for an odd count, -1/4 for even
             use(op.in0);
             use(op.in1);
             use(op.in2);
             def(op.out);
             const uint32_t w =
                 std::max(std::max(ready_br(op.in0), ready_br(op.in1)), ready_br(op.in2));
-            const uint32_t id = new_br(w, op.in0, op.in1, 1, 1, 0u, op.in2, 1);
+            const int32_t k = op.kind == LOCPIR_B200_MAJ ? 1 : -2;
+            const uint32_t id = new_br(w, op.in0, op.in1, k, k, 0u, op.in2, k);
             P.ks[w].push_back({id, SLOT_NONE, 0u, op.out});
             tmps[id].wave_ks = w;
             P.n_ks++;

@@ -723,3 +723,7 @@ class GateEngine:
     def hom_maj(self, a, b, c):
         """3-input majority in one bootstrap (flagged; not in the reference gate set)."""
         return self._emit(_abi.MAJ, self._bit(a), self._bit(b), self._bit(c))
+
+    def hom_xor3(self, a, b, c):
+        """a ^ b ^ c in one bootstrap (flagged; not in the reference gate set)."""
+        return self._emit(_abi.XOR3, self._bit(a), self._bit(b), self._bit(c))

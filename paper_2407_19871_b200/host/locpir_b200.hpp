@@ -120,7 +120,7 @@ private:
 struct GateCounterSnapshot {
     uint64_t and_gates = 0, or_gates = 0, xor_gates = 0, xnor_gates = 0, not_gates = 0,
              mux_gates = 0, nand_gates = 0, nor_gates = 0;
-    uint64_t other_units = 0;  // flagged single-bootstrap gates outside the reference set (MAJ)
+    uint64_t other_units = 0;  // flagged single-bootstrap gates outside the reference set (MAJ, XOR3)
     uint64_t bootstrap_units() const  // gate_engine.hpp:44-48 (+ NAND/NOR)
     {
         return and_gates + or_gates + xor_gates + xnor_gates + nand_gates + nor_gates +
@@ -203,6 +203,11 @@ public:
     CipherBit hom_maj(const CipherBit& a, const CipherBit& b, const CipherBit& c)
     {
         return emit(LOCPIR_B200_MAJ, slot(a), slot(b), slot(c));
+    }
+    // a ^ b ^ c in ONE bootstrap (flagged ternary XOR trees; not in the reference)
+    CipherBit hom_xor3(const CipherBit& a, const CipherBit& b, const CipherBit& c)
+    {
+        return emit(LOCPIR_B200_XOR3, slot(a), slot(b), slot(c));
     }
 
     // the context behind this engine (for BatchingServer and other C-ABI users)

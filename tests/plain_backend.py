@@ -15,6 +15,7 @@ _F = {
     _abi.COPY: lambda a, b, c: a, _abi.ANDNY: lambda a, b, c: (1 - a) & b,
     _abi.ORNY: lambda a, b, c: (1 - a) | b,
     _abi.MAJ: lambda a, b, c: 1 if a + b + c >= 2 else 0,
+    _abi.XOR3: lambda a, b, c: a ^ b ^ c,
 }
 
 

@@ -20,6 +20,7 @@ def interpret(ops, pool):
         _abi.COPY: lambda a, b, c: a, _abi.ANDNY: lambda a, b, c: (1 - a) & b,
         _abi.ORNY: lambda a, b, c: (1 - a) | b,
         _abi.MAJ: lambda a, b, c: 1 if a + b + c >= 2 else 0,
+        _abi.XOR3: lambda a, b, c: a ^ b ^ c,
     }
     for op in ops:
         if op.kind == _abi.CONST:
@@ -30,7 +31,7 @@ def interpret(ops, pool):
     return pool
 
 
-def run_plain(b, folded, xor_tree=True, maj=False):
+def run_plain(b, folded, xor_tree=True, maj=False, tree=False):
     lay = W.PoolLayout(b)
     pool = {}
     l, m = b.l, b.m
@@ -46,7 +47,7 @@ def run_plain(b, folded, xor_tree=True, maj=False):
                 pool[int(lay.bnd[r, k, i])] = int(bb[r, k, i])
         for j in range(m):
             pool[int(lay.svc[r, j])] = int((int(b.payload[r]) >> j) & 1)
-    ops = W.program_ops(b, lay, xor_tree, folded, maj)
+    ops = W.program_ops(b, lay, xor_tree, folded, maj, tree)
     interpret(ops, pool)
     out = np.zeros(b.Q, np.uint64)
     for q in range(b.Q):
@@ -100,3 +101,47 @@ def test_folded_rejects_encrypted_boundaries_and_bad_args():
         W.program_ops(b, W.PoolLayout(b), folded=True)
     with pytest.raises(Exception):
         loc_pir_folded_program(1, 2, 8, 3, [0] * 8, [0] * 8, np.zeros(3), [0] * 6, [0] * 3, 0)
+
+
+def ternary_xor_nodes(R):
+    """Bootstraps of the flagged modes' XOR3 / XOR tree over R leaves (circuits.hpp
+    emit_xor_root with ternary = true)."""
+    nodes = 0
+    while R > 1:
+        nodes += R // 3 + (R % 3 == 2)
+        R = R // 3 + (R % 3 != 0)
+    return nodes
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 4, 5, 9, 10])
+@pytest.mark.parametrize("xor_tree", [0, 1])
+def test_flagged_modes_skip_the_enc0_xor(R, xor_tree):
+    """Flagged modes drop the bootstrapped XOR with Enc(0) that starts each bit column in
+    the reference (circuits.hpp:257-261) and, with the tree, reduce a column with XOR3
+    nodes (ceil(log3 R) levels); the plaintext answers are the reference function's."""
+    l, m, Q = 6, 3, 3
+    b = W.make_batch(Q, R, l, m, seed=40 + R)
+    for q in range(min(Q, R)):
+        b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
+        b.y[q] = (b.boxes[q, 2] + b.boxes[q, 3]) // 2
+    lay = W.PoolLayout(b)
+    ref = plan(W.program_ops(b, lay, xor_tree, folded=False))
+    assert ref["blind_rotations"] == b.units()
+    want = Q * m * (ternary_xor_nodes(R) if xor_tree else R - 1)
+    for kw in (dict(folded=True), dict(folded=True, tree=True), dict(maj=True), dict(tree=True)):
+        ops = W.program_ops(b, lay, xor_tree, **kw)
+        xors = sum(1 for o in ops if o.kind in (_abi.XOR, _abi.XOR3))
+        assert xors == want, kw
+        got, _ = run_plain(b, kw.get("folded", False), xor_tree, kw.get("maj", False),
+                           kw.get("tree", False))
+        assert np.array_equal(got, b.truth()), kw
+
+
+def test_ternary_xor_tree_depth():
+    """R = 256 boxes (cfg3): 6 XOR levels instead of the binary tree's 8 + 1."""
+    b = W.make_batch(1, 256, 4, 1, seed=9)
+    lay = W.PoolLayout(b)
+    f = plan(W.program_ops(b, lay, True, folded=True))
+    r = plan(W.program_ops(b, lay, True, folded=False))
+    assert ternary_xor_nodes(256) == 129  # 85 + 29 + 10 + 3 + 1 + 1, six levels
+    assert f["blind_rotations"] < r["blind_rotations"]

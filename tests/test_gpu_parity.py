@@ -447,7 +447,7 @@ def _random_program(rng, n_inputs, n_ops, first_slot):
     """Random SSA gate DAG over n_inputs input slots; returns (ops, plaintext evaluator)."""
     from paper_2407_19871_b200 import _abi
     kinds = [_abi.AND, _abi.OR, _abi.XOR, _abi.XNOR, _abi.NAND, _abi.NOR, _abi.MUX, _abi.NOT,
-             _abi.COPY, _abi.CONST, _abi.ANDNY, _abi.ORNY, _abi.MAJ]
+             _abi.COPY, _abi.CONST, _abi.ANDNY, _abi.ORNY, _abi.MAJ, _abi.XOR3]
     live = list(range(n_inputs))
     ops = []
     nxt = first_slot
@@ -474,6 +474,8 @@ def _eval_plain(ops, vals):
             v[o] = f[k](v[a], v[b])
         elif k == _abi.MAJ:
             v[o] = 1 if v[a] + v[b] + v[c] >= 2 else 0
+        elif k == _abi.XOR3:
+            v[o] = v[a] ^ v[b] ^ v[c]
         elif k == _abi.MUX:
             v[o] = v[b] if v[a] else v[c]
         elif k == _abi.NOT:
@@ -633,8 +635,9 @@ def test_program_graph_replay_survives_pool_growth(dev):
 
 @pytest.mark.parametrize("level", [80, 128])
 def test_flagged_gate_forms_on_the_throughput_kernel(dev, level, okeys80, okeys128):
-    """MAJ (3-input prologue), ANDNY and ORNY with more bootstraps per level than SMs, so
-    the throughput kernel (not the latency kernel) runs them: bit-exact with the oracle."""
+    """MAJ and XOR3 (3-input prologue), ANDNY and ORNY with more bootstraps per level than
+    SMs, so the throughput kernel (not the latency kernel) runs them: bit-exact with the
+    oracle."""
     from paper_2407_19871_b200 import _abi
     p, keys, ctx = dev[level]
     ok = okeys80 if level == 80 else okeys128
@@ -642,20 +645,21 @@ def test_flagged_gate_forms_on_the_throughput_kernel(dev, level, okeys80, okeys1
     rng = np.random.default_rng(level + 7)
     bits = rng.integers(0, 2, (3, G)).astype(np.uint8)
     cts = [keys.encrypt_bits(bits[i], 70 + i) for i in range(3)]
-    ctx.pool_reserve(6 * G)
+    ctx.pool_reserve(7 * G)
     for i in range(3):
         ctx.h2d(i * G, cts[i])
     ops = [(_abi.MAJ, g, G + g, 2 * G + g, 3 * G + g) for g in range(G)]
     ops += [(_abi.ANDNY, g, G + g, _abi.SLOT_NONE, 4 * G + g) for g in range(G)]
     ops += [(_abi.ORNY, g, G + g, _abi.SLOT_NONE, 5 * G + g) for g in range(G)]
+    ops += [(_abi.XOR3, g, G + g, 2 * G + g, 6 * G + g) for g in range(G)]
     ctx.run(ops)
     a, b, c = bits
     for base, want, kind in ((3, (a.astype(int) + b + c >= 2), "maj"), (4, (1 - a) & b, "andny"),
-                             (5, (1 - a) | b, "orny")):
+                             (5, (1 - a) | b, "orny"), (6, a ^ b ^ c, "xor3")):
         got = ctx.d2h(base * G, G)
         assert list(keys.decrypt_bits(got)) == list(np.asarray(want, np.uint8)), kind
         for g in (0, G - 1):
-            args = (cts[0][g], cts[1][g], cts[2][g]) if kind == "maj" else (cts[0][g], cts[1][g])
+            args = (cts[0][g], cts[1][g], cts[2][g]) if kind in ("maj", "xor3") else (cts[0][g], cts[1][g])
             assert np.array_equal(got[g], ok.gate(kind, *args)), kind
 
 

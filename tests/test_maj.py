@@ -41,9 +41,12 @@ def test_maj_unit_count_and_depth(l, m):
     lay = W.PoolLayout(b)
     mj = plan(W.program_ops(b, lay, True, False, True))
     ref = plan(W.program_ops(b, lay, True, False, False))
-    assert mj["blind_rotations"] == b.Q * b.R * (4 * l + 2 * m + 3)
+    # flagged modes: per region 4l comparator + 3 AND + m mask bootstraps; each bit column
+    # is a ternary XOR3 tree without the reference's XOR with Enc(0)
+    from test_folded import ternary_xor_nodes
+    assert mj["blind_rotations"] == b.Q * (b.R * (4 * l + m + 3) + m * ternary_xor_nodes(b.R))
     assert ref["blind_rotations"] == b.units()
-    assert mj["levels"] <= ref["levels"]
+    assert mj["levels"] < ref["levels"]
 
 
 def test_oracle_majority_gate_truth_table():
@@ -54,6 +57,18 @@ def test_oracle_majority_gate_truth_table():
             for c in (0, 1):
                 out = K.gate("maj", K.encrypt(a, s), K.encrypt(b, s), K.encrypt(c, s))
                 assert K.decrypt(out) == int(a + b + c >= 2)
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_oracle_xor3_gate_truth_table(level):
+    """XOR3 = BS(-2 (a + b + c)): odd counts land on +1/4, even on -1/4 (mod 1)."""
+    K = O.TfheKeys(level, 3)
+    s = O.NoiseSampler(5, K.p.alpha_in)
+    for a in (0, 1):
+        for b in (0, 1):
+            for c in (0, 1):
+                out = K.gate("xor3", K.encrypt(a, s), K.encrypt(b, s), K.encrypt(c, s))
+                assert K.decrypt(out) == a ^ b ^ c
 
 
 @pytest.mark.gpu
@@ -68,14 +83,19 @@ def test_maj_gates_bit_exact_and_loc_pir_encrypted(level, okeys80, okeys128):
     rng = np.random.default_rng(level)
     bits = rng.integers(0, 2, (3, 64)).astype(np.uint8)
     cts = [keys.encrypt_bits(bits[i], 50 + i) for i in range(3)]
-    ctx.pool_reserve(4 * 64)
+    ctx.pool_reserve(5 * 64)
     for i in range(3):
         ctx.h2d(64 * i, cts[i])
-    ctx.run([(_abi.MAJ, g, 64 + g, 128 + g, 192 + g) for g in range(64)])
+    # one level of 128 (< #SMs): the latency kernel
+    ctx.run([(_abi.MAJ, g, 64 + g, 128 + g, 192 + g) for g in range(64)] +
+            [(_abi.XOR3, g, 64 + g, 128 + g, 256 + g) for g in range(64)])
     got = ctx.d2h(192, 64)
     assert list(keys.decrypt_bits(got)) == list((bits.sum(0) >= 2).astype(np.uint8))
+    got3 = ctx.d2h(256, 64)
+    assert list(keys.decrypt_bits(got3)) == list(bits[0] ^ bits[1] ^ bits[2])
     for g in (0, 63):
         assert np.array_equal(got[g], ok.gate("maj", cts[0][g], cts[1][g], cts[2][g]))
+        assert np.array_equal(got3[g], ok.gate("xor3", cts[0][g], cts[1][g], cts[2][g]))
     b = W.make_batch(3, 6, 32, 4, seed=level, encrypted_bounds=True)
     for q in range(3):
         b.x[q] = (b.boxes[q, 0] + b.boxes[q, 1]) // 2
@@ -87,6 +107,8 @@ def test_maj_gates_bit_exact_and_loc_pir_encrypted(level, okeys80, okeys128):
     prog = W.program(ctx, b, lay, maj=True)
     prog.launch()
     assert np.array_equal(W.read_results(ctx, keys, b, lay), b.truth())
-    assert ctx.counters()["bootstrap_units"] == b.Q * b.R * (4 * 32 + 2 * 4 + 3)
+    from test_folded import ternary_xor_nodes
+    assert ctx.counters()["bootstrap_units"] == b.Q * (b.R * (4 * 32 + 4 + 3) +
+                                                       4 * ternary_xor_nodes(b.R))
     prog.close()
     ctx.close()
