@@ -576,19 +576,22 @@ def device_ms(fn, reps=3, warm=True):
 
 
 def latency_floor(ctx, keys, levels, measured_ms):
-    """cfg1 is latency-bound (a 21-level circuit with <= 64 gates per level): its roof is
-    levels x the latency of ONE bootstrapped gate (blind rotation on the latency kernel
-    K1l + split key switch K2s), measured here with a one-gate program."""
+    """cfg1 is latency-bound (a 21-level circuit with <= 68 gates per level): its roof is
+    the device time of a chain of `levels` dependent bootstrapped gates (one gate per
+    level, the same latency kernels K1l + K2s and the same graph-replayed launch sequence
+    as the circuit), i.e. critical-path levels x one level's latency."""
     from paper_2407_19871_b200 import _abi
-    ctx.pool_reserve(4)
+    ctx.pool_reserve(levels + 2)
     ctx.h2d(0, keys.encrypt_bits(np.array([1, 0], np.uint8), 5))
-    prog = ctx.program([(_abi.NAND, 0, 1, _abi.SLOT_NONE, 2)])
-    t_gate = device_ms(prog.launch, reps=5)
+    chain = [(_abi.NAND, 0, 1, _abi.SLOT_NONE, 2)]
+    chain += [(_abi.NAND, 1 + i, 0, _abi.SLOT_NONE, 2 + i) for i in range(1, levels)]
+    prog = ctx.program(chain)
+    t_chain = device_ms(prog.launch, reps=5)
     prog.close()
-    floor = levels * t_gate
-    return {"bound": "latency", "levels": levels, "one_gate_ms": t_gate, "floor_ms": floor,
-            "measured_ms": measured_ms, "frac": floor / measured_ms,
-            "note": "floor = critical-path levels x one bootstrapped gate's device latency"}
+    return {"bound": "latency", "levels": levels, "one_gate_ms": t_chain / levels,
+            "floor_ms": t_chain, "measured_ms": measured_ms, "frac": t_chain / measured_ms,
+            "note": "floor = device time of a chain of `levels` dependent bootstrapped gates "
+                    "(critical-path levels x one level's latency)"}
 
 
 def run_shard_emulation(ctx, keys, Ns=(2, 4, 8)):

@@ -163,7 +163,7 @@ int locpir_b200_program_prepare(locpir_b200_ctx* ctx, locpir_b200_program* prog)
 uint64_t locpir_b200_program_kernels(const locpir_b200_program* prog);
 void locpir_b200_program_destroy(locpir_b200_program* prog);
 
-/* Host-only plan of a program (no GPU): number of levels, blind rotations,
+/* Host-only plan of a program (no GPU): number of bootstrap levels, blind rotations,
  * key switches; used by tests and the C++ mirror. */
 int locpir_b200_plan(const locpir_b200_gate_op* ops, uint64_t count, uint32_t* levels,
                      uint64_t* blind_rotations, uint64_t* key_switches);

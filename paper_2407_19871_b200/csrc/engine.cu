@@ -955,8 +955,12 @@ int locpir_b200_plan(const locpir_b200_gate_op* ops, uint64_t count, uint32_t* l
 {
     try {
         Plan P = build_plan(ops, count);
-        if (levels)
-            *levels = P.waves();
+        if (levels) {  // bootstrap levels (a trailing wave of free linear ops is not one)
+            uint32_t lv = 0;
+            for (uint32_t w = 0; w < P.waves(); w++)
+                lv += !P.br[w].empty();
+            *levels = lv;
+        }
         if (blind_rotations)
             *blind_rotations = P.n_br;
         if (key_switches)
