@@ -60,6 +60,24 @@ def main():
     assert np.array_equal(W.read_results(ctx, keys, bt, lay), bt.truth())
     h.update(ctx.d2h(int(lay.out.min()), bt.Q * bt.m).tobytes())
     prog.close()
+    # the flagged folded mode (ANDNY / ORNY chains, ternary XOR3 sums) and a level of the
+    # 3-input gates MAJ / XOR3 (the 3-input prologue)
+    prog = W.program(ctx, bt, lay, folded=True)
+    prog.launch()
+    assert np.array_equal(W.read_results(ctx, keys, bt, lay), bt.truth())
+    h.update(ctx.d2h(int(lay.out.min()), bt.Q * bt.m).tobytes())
+    prog.close()
+    G3 = 200
+    base = lay.total - 4 * G3
+    C3 = rng.integers(0, 2, (3, G3)).astype(np.uint8)
+    for i in range(3):
+        ctx.h2d(base + i * G3, keys.encrypt_bits(C3[i], 60 + i))
+    ctx.run([(_abi.MAJ if g % 2 else _abi.XOR3, base + g, base + G3 + g, base + 2 * G3 + g,
+              base + 3 * G3 + g) for g in range(G3)])
+    out3 = ctx.d2h(base + 3 * G3, G3)
+    want3 = np.where(np.arange(G3) % 2 == 1, (C3.sum(0) >= 2).astype(np.uint8), C3[0] ^ C3[1] ^ C3[2])
+    assert np.array_equal(keys.decrypt_bits(out3), want3)
+    h.update(out3.tobytes())
     # the batcher's wire kernels (K5)
     l, m = 8, 3
     boxes = np.array([[0, 20, 0, 20], [-10, 5, -10, 5]], np.int64)
