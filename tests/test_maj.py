@@ -112,3 +112,24 @@ def test_maj_gates_bit_exact_and_loc_pir_encrypted(level, okeys80, okeys128):
                                                        4 * ternary_xor_nodes(b.R))
     prog.close()
     ctx.close()
+
+
+def test_three_input_gate_noise_margins():
+    """Noise budget of the flagged 3-input gates at the noisier 80-bit set: bootstrapped
+    outputs have std sigma; MAJ sums three of them (margin 1/8, std sqrt(3) sigma) and XOR3
+    -2x three of them (margin 1/4, std 2 sqrt(3) sigma) -- both >= 15 sigma from a decision
+    boundary, as is the reference's 2-input XOR (margin 1/4, 2 sqrt(2) sigma)."""
+    K = O.TfheKeys(80, 3)
+    s = O.NoiseSampler(4, K.p.alpha_in)
+    rng = np.random.default_rng(80)
+    G = 240
+    A, B = rng.integers(0, 2, G), rng.integers(0, 2, G)
+    a = np.stack([K.encrypt(int(x), s) for x in A])
+    b = np.stack([K.encrypt(int(x), s) for x in B])
+    out = K.gate_batch("nand", a, b, O.FFT, 8)
+    n = K.n
+    ph = (out[:, n].astype(np.int64) - out[:, :n].astype(np.int64) @ K.lwe_key.astype(np.int64))
+    ph = (((ph + 2 ** 31) % 2 ** 32) - 2 ** 31) / 2 ** 32
+    sigma = (ph - np.where(1 - (A & B), 0.125, -0.125)).std()
+    assert 0.125 / (np.sqrt(3) * sigma) > 15
+    assert 0.25 / (2 * np.sqrt(3) * sigma) > 15
