@@ -110,8 +110,16 @@ def lib():
                                    C.c_int]
         L.or_gate_batch.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p, C.c_uint64,
                                     C.c_int, C.c_int]
+        L.or_gate_batch_simd.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p,
+                                         C.c_uint64, C.c_int]
+        L.or_simd_lanes.restype = C.c_int
         _lib = L
     return _lib
+
+
+def simd_lanes() -> int:
+    """Ciphertexts per SIMD lane group of gate_batch_simd (8 with AVX-512, 4 with AVX2)."""
+    return int(lib().or_simd_lanes())
 
 
 def _u32(a):
@@ -276,6 +284,19 @@ class TfheKeys:
                                  a.shape[0], mode, threads)
         if rc:
             raise ValueError(f"oracle gate batch failed: {rc}")
+        return out
+
+    def gate_batch_simd(self, kind: str, a: np.ndarray, b: np.ndarray,
+                        threads: int = 1) -> np.ndarray:
+        """FFT-mode 2-input gates, 4 ciphertexts per AVX2 lane group: bit-identical to
+        gate_batch(kind, a, b, FFT) (the CPU baseline's fast path)."""
+        a = np.ascontiguousarray(a, np.uint32)
+        b = np.ascontiguousarray(b, np.uint32)
+        out = np.zeros_like(a)
+        rc = lib().or_gate_batch_simd(C.byref(self.ks), GATES[kind], _u32(a), _u32(b),
+                                      _u32(out), a.shape[0], threads)
+        if rc:
+            raise ValueError(f"oracle simd gate batch failed: {rc}")
         return out
 
     def blind_rotate_extract(self, lwe: np.ndarray, mu: int = 0x20000000,

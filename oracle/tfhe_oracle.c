@@ -993,3 +993,342 @@ void or_cb_encrypt(const uint8_t* key, uint32_t n, uint64_t seed, uint32_t first
         o[n] = dot + mus[j] + cb_noise(seed, idx, alpha);
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Lane-batched FFT-mode gates (CPU baseline speed; same arithmetic)         */
+/* ------------------------------------------------------------------------ */
+/* or_gate_batch_simd: the FFT-mode gate of or_gate for VL ciphertexts at a time, one per
+ * SIMD lane (VL = 8 with AVX-512, 4 with AVX2).  Every lane executes exactly the scalar
+ * operation sequence (the same fma / mul / add per element, the same tables,
+ * round-to-nearest-even), so the results are bit-identical to or_gate(..., ORACLE_FFT,
+ * ...) -- tested.  The bootstrapping-key row of step i is shared by the lanes (broadcast)
+ * and the transforms run on VL-wide vectors.  It exists so the CPU baseline is not
+ * handicapped by a scalar port. */
+#include <immintrin.h>
+
+#ifdef __AVX512F__
+#define OR_LANES 8
+typedef __m512d vd;
+typedef __m256i vu; /* OR_LANES x u32 */
+#define VSET1 _mm512_set1_pd
+#define VFMA _mm512_fmadd_pd
+#define VADD _mm512_add_pd
+#define VSUB _mm512_sub_pd
+#define VMUL _mm512_mul_pd
+#define VNEG(x) _mm512_xor_pd((x), _mm512_set1_pd(-0.0))
+#define VCVT_I32 _mm512_cvtepi32_pd
+#define ULOAD(p) _mm256_loadu_si256((const __m256i*)(p))
+#define USTORE(p, x) _mm256_storeu_si256((__m256i*)(p), (x))
+#define UADD _mm256_add_epi32
+#define USUB _mm256_sub_epi32
+#define UAND _mm256_and_si256
+#define USET1 _mm256_set1_epi32
+#define USRL _mm256_srl_epi32
+/* llrint(r) mod 2^32 per lane: round to nearest even, exact int64, low word */
+static inline vu low32_rint(vd r)
+{
+    return _mm512_cvtepi64_epi32(
+        _mm512_cvtpd_epi64(_mm512_roundscale_pd(r, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC)));
+}
+#else
+#define OR_LANES 4
+typedef __m256d vd;
+typedef __m128i vu;
+#define VSET1 _mm256_set1_pd
+#define VFMA _mm256_fmadd_pd
+#define VADD _mm256_add_pd
+#define VSUB _mm256_sub_pd
+#define VMUL _mm256_mul_pd
+#define VNEG(x) _mm256_xor_pd((x), _mm256_set1_pd(-0.0))
+#define VCVT_I32 _mm256_cvtepi32_pd
+#define ULOAD(p) _mm_loadu_si128((const __m128i*)(p))
+#define USTORE(p, x) _mm_storeu_si128((__m128i*)(p), (x))
+#define UADD _mm_add_epi32
+#define USUB _mm_sub_epi32
+#define UAND _mm_and_si128
+#define USET1 _mm_set1_epi32
+#define USRL _mm_srl_epi32
+static inline vu low32_rint(vd x)
+{
+    /* round to nearest even; |r| < 2^51: low word of r + 1.5 * 2^52, else lane by lane */
+    const vd r = _mm256_round_pd(x, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+    const vd ab = _mm256_andnot_pd(_mm256_set1_pd(-0.0), r);
+    if (_mm256_movemask_pd(_mm256_cmp_pd(ab, _mm256_set1_pd(2251799813685248.0), _CMP_GE_OQ)) == 0) {
+        const __m256i bits = _mm256_castpd_si256(_mm256_add_pd(r, _mm256_set1_pd(6755399441055744.0)));
+        return _mm256_castsi256_si128(
+            _mm256_permutevar8x32_epi32(bits, _mm256_setr_epi32(0, 2, 4, 6, 0, 2, 4, 6)));
+    }
+    double d[4];
+    _mm256_storeu_pd(d, r);
+    return _mm_setr_epi32((int)(uint32_t)(uint64_t)(int64_t)d[0], (int)(uint32_t)(uint64_t)(int64_t)d[1],
+                          (int)(uint32_t)(uint64_t)(int64_t)d[2], (int)(uint32_t)(uint64_t)(int64_t)d[3]);
+}
+#endif
+
+static inline void vbf_ct(vd* ur, vd* ui, vd* vr, vd* vi, vd c, vd nc, vd t, int rot)
+{
+    vd xr = *vr, xi = *vi;
+    if (rot == 1) {
+        const vd tmp = xr;
+        xr = VNEG(xi);
+        xi = tmp;
+    } else if (rot == 3) {
+        const vd tmp = xr;
+        xr = xi;
+        xi = VNEG(tmp);
+    }
+    const vd sr = VFMA(VNEG(xi), t, xr), si = VFMA(xr, t, xi);
+    const vd a = *ur, b = *ui;
+    *ur = VFMA(c, sr, a);
+    *ui = VFMA(c, si, b);
+    *vr = VFMA(nc, sr, a);
+    *vi = VFMA(nc, si, b);
+}
+
+/* cmul: re = fma(x.re, w.re, -(x.im * w.im)), im = fma(x.re, w.im, x.im * w.re) */
+static inline void vcmul(vd xr, vd xi, vd wr, vd wi, vd* rr, vd* ri)
+{
+    *rr = VFMA(xr, wr, VNEG(VMUL(xi, wi)));
+    *ri = VFMA(xr, wi, VMUL(xi, wr));
+}
+
+static void vfwd_soa(const fft2_tab* T, vd* zr, vd* zi)
+{
+    const uint32_t M = OR_M;
+    for (uint32_t s = 0; s < 9; s++) {
+        const uint32_t h = M >> (s + 1);
+        for (uint32_t b = 0; b < (1u << s); b++) {
+            const int sib = (s % 3 != 0) && (b & 1);
+            const uint32_t v = (1u << s) + b - (sib ? 1 : 0);
+            const vd c = VSET1(T->fc[v]), nc = VSET1(-T->fc[v]), t = VSET1(T->ft[v]);
+            const uint32_t o = 2 * h * b;
+            for (uint32_t j = 0; j < h; j++)
+                vbf_ct(&zr[o + j], &zi[o + j], &zr[o + j + h], &zi[o + j + h], c, nc, t, sib ? 1 : 0);
+        }
+    }
+}
+
+static void vinv_soa(const fft2_tab* T, vd* zr, vd* zi)
+{
+    const uint32_t M = OR_M;
+    for (uint32_t h = 1; h < M; h <<= 1) {
+        const uint32_t step = (M / 2) / h;
+        for (uint32_t o = 0; o < M; o += 2 * h)
+            for (uint32_t j = 0; j < h; j++) {
+                const uint32_t e = j * step;
+                vd *ur = &zr[o + j], *ui = &zi[o + j], *vr = &zr[o + j + h], *vi = &zi[o + j + h];
+                if (h <= 4 && e == 0) { /* bf_1 */
+                    const vd a = *ur, b = *ui, c = *vr, d = *vi;
+                    *ur = VADD(a, c);
+                    *ui = VADD(b, d);
+                    *vr = VSUB(a, c);
+                    *vi = VSUB(b, d);
+                } else if (h <= 4 && e == M / 4) { /* bf_mi: -i v = (vi, -vr) */
+                    const vd a = *ur, b = *ui, c = *vi, d = VNEG(*vr);
+                    *ur = VADD(a, c);
+                    *ui = VADD(b, d);
+                    *vr = VSUB(a, c);
+                    *vi = VSUB(b, d);
+                } else if (h == 8 || h == 64) { /* bf_std with conj(W[e]) */
+                    vd tr, ti;
+                    vcmul(*vr, *vi, VSET1(T->W[e][0]), VSET1(-T->W[e][1]), &tr, &ti);
+                    const vd a = *ur, b = *ui;
+                    *ur = VADD(a, tr);
+                    *ui = VADD(b, ti);
+                    *vr = VSUB(a, tr);
+                    *vi = VSUB(b, ti);
+                } else {
+                    const uint32_t e0 = e % (M / 4);
+                    vbf_ct(ur, ui, vr, vi, VSET1(T->ic[e0]), VSET1(-T->ic[e0]), VSET1(-T->it[e0]),
+                           e >= M / 4 ? 3 : 0);
+                }
+            }
+    }
+}
+
+typedef struct {
+    vd Fr[OR_M], Fi[OR_M];
+    vd Ar[2][OR_M], Ai[2][OR_M];
+    uint32_t tmp[2][OR_N][OR_LANES]; /* (X^a - 1) ACC, lane-interleaved */
+    uint32_t acc[2][OR_N][OR_LANES]; /* ACC, lane-interleaved */
+} simd_ws;
+
+/* FFT-mode blind rotation + extraction of `lanes` (<= OR_LANES) combined LWE samples */
+static void blind_rotate_extract_lanes(const or_keyset* ks, const uint32_t* const* lwe, int lanes,
+                                       uint32_t mu, simd_ws* W, uint32_t* const* out_N)
+{
+    const or_params* p = &ks->p;
+    const uint32_t n = p->n, N = p->N, M = N / 2, rows = (p->k + 1) * p->l;
+    const fft2_tab* tab = get_tab(N);
+    const uint32_t doff = decomp_offset(p);
+    const uint32_t dmask = (1u << p->bgbit) - 1;
+    const int32_t dhalf = 1 << (p->bgbit - 1);
+    memset(W->acc, 0, sizeof(W->acc));
+    for (int L = 0; L < lanes; L++) { /* ACC = (0, X^{-bbar} mu sum X^j) */
+        const uint32_t e = (2 * N - or_mod_switch(lwe[L][n], N)) % (2 * N);
+        for (uint32_t j = 0; j < N; j++) {
+            const uint32_t idx = (j - e) & (2 * N - 1);
+            W->acc[1][j][L] = idx < N ? mu : 0u - mu;
+        }
+    }
+    for (uint32_t i = 0; i < n; i++) {
+        uint32_t a[OR_LANES];
+        int any = 0;
+        int32_t lv[OR_LANES];
+        for (int L = 0; L < OR_LANES; L++) {
+            a[L] = L < lanes ? or_mod_switch(lwe[L][i], N) : 0;
+            any |= a[L] != 0;
+            lv[L] = a[L] ? -1 : 0; /* lanes whose external product is added (or_blind_rotate_acc skips a = 0) */
+        }
+        if (!any)
+            continue;
+        const vu live = ULOAD(lv);
+        for (int L = 0; L < OR_LANES; L++)
+            for (uint32_t c = 0; c < 2; c++)
+                for (uint32_t j = 0; j < N; j++) { /* (X^a P)_j - P_j, a in [0, 2N) */
+                    const uint32_t idx = (j - a[L]) & (2 * N - 1);
+                    const uint32_t pv = W->acc[c][idx & (N - 1)][L];
+                    W->tmp[c][j][L] = (idx < N ? pv : 0u - pv) - W->acc[c][j][L];
+                }
+        memset(W->Ar, 0, sizeof(W->Ar));
+        memset(W->Ai, 0, sizeof(W->Ai));
+        for (uint32_t c = 0; c < 2; c++)
+            for (uint32_t q = 0; q < p->l; q++) {
+                /* or_decompose lane-wise: ((x + off) >> shift) & mask - half, then exact (double) */
+                const vu voff = USET1((int)doff), vmask = USET1((int)dmask), vhalf = USET1(dhalf);
+                const __m128i vsh = _mm_cvtsi32_si128((int)(32 - (q + 1) * p->bgbit));
+                for (uint32_t j = 0; j < M; j++) {
+                    const vu d0 = USUB(UAND(USRL(UADD(ULOAD(W->tmp[c][j]), voff), vsh), vmask), vhalf);
+                    const vu d1 = USUB(UAND(USRL(UADD(ULOAD(W->tmp[c][j + M]), voff), vsh), vmask), vhalf);
+                    W->Fr[j] = VCVT_I32(d0);
+                    W->Fi[j] = VCVT_I32(d1);
+                }
+                vfwd_soa(tab, W->Fr, W->Fi);
+                const uint32_t r = c * p->l + q;
+                for (uint32_t comp = 0; comp < 2; comp++) {
+                    const double* Br = ks->bk_fft_soa + (((size_t)i * rows + r) * 2 + comp) * N;
+                    const double* Bi = Br + M;
+                    vd* ar = W->Ar[comp];
+                    vd* ai = W->Ai[comp];
+                    for (uint32_t f = 0; f < M; f++) {
+                        const vd br = VSET1(Br[f]), bi = VSET1(Bi[f]);
+                        vd re = VFMA(W->Fr[f], br, ar[f]);
+                        re = VFMA(VNEG(W->Fi[f]), bi, re);
+                        vd im = VFMA(W->Fr[f], bi, ai[f]);
+                        im = VFMA(W->Fi[f], br, im);
+                        ar[f] = re;
+                        ai[f] = im;
+                    }
+                }
+            }
+        for (uint32_t comp = 0; comp < 2; comp++) {
+            vd* zr = W->Ar[comp];
+            vd* zi = W->Ai[comp];
+            vinv_soa(tab, zr, zi);
+            for (uint32_t j = 0; j < M; j++) { /* untwist, round, ACC += (a != 0 lanes) */
+                vd wr, wi;
+                vcmul(zr[j], zi[j], VSET1(tab->TW[j][0]), VSET1(-tab->TW[j][1]), &wr, &wi);
+                uint32_t* a0 = W->acc[comp][j];
+                uint32_t* a1 = W->acc[comp][j + M];
+                USTORE(a0, UADD(ULOAD(a0), UAND(low32_rint(wr), live)));
+                USTORE(a1, UADD(ULOAD(a1), UAND(low32_rint(wi), live)));
+            }
+        }
+    }
+    for (int L = 0; L < lanes; L++) { /* sample extraction at index 0 */
+        uint32_t* o = out_N[L];
+        o[0] = W->acc[0][0][L];
+        for (uint32_t j = 1; j < N; j++)
+            o[j] = 0u - W->acc[0][N - j][L];
+        o[N] = W->acc[1][0][L];
+    }
+}
+
+typedef struct {
+    const or_keyset* ks;
+    int kind;
+    const uint32_t *a, *b;
+    uint32_t* out;
+    uint64_t lo, hi;
+    int rc;
+} simd_job;
+
+static void* simd_worker(void* arg)
+{
+    simd_job* jb = (simd_job*)arg;
+    const or_keyset* ks = jb->ks;
+    const uint32_t n = ks->p.n, N = ks->p.N;
+    const size_t w = n + 1;
+    simd_ws* W = (simd_ws*)aligned_alloc(64, (sizeof(simd_ws) + 63) / 64 * 64);
+    uint32_t* comb = (uint32_t*)malloc(sizeof(uint32_t) * w * OR_LANES);
+    uint32_t* ext = (uint32_t*)malloc(sizeof(uint32_t) * (N + 1) * OR_LANES);
+    for (uint64_t g0 = jb->lo; g0 < jb->hi; g0 += OR_LANES) {
+        const int lanes = (int)(jb->hi - g0 < OR_LANES ? jb->hi - g0 : OR_LANES);
+        const uint32_t* lw[OR_LANES];
+        uint32_t* eo[OR_LANES];
+        for (int L = 0; L < OR_LANES; L++) {
+            lw[L] = comb + (size_t)L * w;
+            eo[L] = ext + (size_t)L * (N + 1);
+        }
+        for (int L = 0; L < lanes; L++) {
+            const uint32_t* A = jb->a + (g0 + L) * w;
+            const uint32_t* B = jb->b + (g0 + L) * w;
+            uint32_t* cb = comb + (size_t)L * w;
+            switch (jb->kind) {
+            case OR_GATE_AND: lin2(n, 0xE0000000u, 1, A, 1, B, cb); break;
+            case OR_GATE_OR: lin2(n, 0x20000000u, 1, A, 1, B, cb); break;
+            case OR_GATE_XOR: lin2(n, 0x40000000u, 2, A, 2, B, cb); break;
+            case OR_GATE_XNOR: lin2(n, 0xC0000000u, -2, A, -2, B, cb); break;
+            case OR_GATE_NAND: lin2(n, 0x20000000u, -1, A, -1, B, cb); break;
+            case OR_GATE_NOR: lin2(n, 0xE0000000u, -1, A, -1, B, cb); break;
+            default: jb->rc = -1; goto out;
+            }
+        }
+        blind_rotate_extract_lanes(ks, lw, lanes, 0x20000000u, W, eo);
+        for (int L = 0; L < lanes; L++)
+            or_keyswitch(ks, eo[L], jb->out + (g0 + L) * w);
+    }
+out:
+    free(W);
+    free(comb);
+    free(ext);
+    return NULL;
+}
+
+int or_simd_lanes(void) { return OR_LANES; }
+
+int or_gate_batch_simd(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
+                       uint32_t* out, uint64_t count, int threads)
+{
+    if (ks->p.N != OR_N)
+        return -1;
+    if (threads < 1)
+        threads = 1;
+    const uint64_t groups = (count + OR_LANES - 1) / OR_LANES;
+    if ((uint64_t)threads > groups)
+        threads = groups ? (int)groups : 1;
+    simd_job* jobs = (simd_job*)calloc(threads, sizeof(simd_job));
+    pthread_t* tid = (pthread_t*)calloc(threads, sizeof(pthread_t));
+    const uint64_t chunk = (groups + threads - 1) / threads * OR_LANES; /* whole lane groups */
+    for (int t = 0; t < threads; t++) {
+        jobs[t].ks = ks;
+        jobs[t].kind = kind;
+        jobs[t].a = a;
+        jobs[t].b = b;
+        jobs[t].out = out;
+        jobs[t].lo = (uint64_t)t * chunk < count ? (uint64_t)t * chunk : count;
+        jobs[t].hi = jobs[t].lo + chunk < count ? jobs[t].lo + chunk : count;
+    }
+    for (int t = 1; t < threads; t++)
+        pthread_create(&tid[t], NULL, simd_worker, &jobs[t]);
+    simd_worker(&jobs[0]);
+    int rc = jobs[0].rc;
+    for (int t = 1; t < threads; t++) {
+        pthread_join(tid[t], NULL);
+        if (jobs[t].rc)
+            rc = jobs[t].rc;
+    }
+    free(jobs);
+    free(tid);
+    return rc;
+}

@@ -160,6 +160,12 @@ int or_gate(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
  * parallel.hpp:15-52).  a,b,out are [count][n+1]. */
 int or_gate_batch(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
                   uint32_t* out, uint64_t count, int mode, int threads);
+/* The same FFT-mode 2-input gates, or_simd_lanes() ciphertexts per SIMD lane group (8 with
+ * AVX-512, 4 with AVX2; bit-identical to or_gate_batch(..., ORACLE_FFT, ...)); the CPU
+ * baseline's fast path. */
+int or_simd_lanes(void);
+int or_gate_batch_simd(const or_keyset* ks, int kind, const uint32_t* a, const uint32_t* b,
+                       uint32_t* out, uint64_t count, int threads);
 
 /* Counter-based client encryption (paper_2407_19871_b200/csrc/cbrng.h):
  * sample j = (mask philox words, body = <a, key> + mus[j] + noise) with stream index

@@ -164,3 +164,22 @@ def test_avx512_baseline_build_is_bit_identical():
     if " avx512f" not in open("/proc/cpuinfo").read() or not os.path.exists(v4):
         pytest.skip("no AVX-512 host or no v4 build")
     assert _gate_digest(v4) == _gate_digest(None)
+
+
+@pytest.mark.parametrize("level", [80, 128])
+def test_lane_batched_oracle_is_bit_identical(level):
+    """oracle gate_batch_simd (the CPU baseline's fast path: one ciphertext per SIMD lane,
+    8 per AVX-512 / 4 per AVX2 vector) reproduces the scalar FFT-mode gates bit for bit,
+    including a partial lane group and lanes whose a_i = 0 steps are skipped."""
+    from oracle import oracle as O
+    K = O.TfheKeys(level, 21)
+    s = O.NoiseSampler(22, K.p.alpha_in)
+    G = O.simd_lanes() + 3
+    rng = np.random.default_rng(level)
+    A, B = rng.integers(0, 2, G), rng.integers(0, 2, G)
+    a = np.stack([K.encrypt(int(x), s) for x in A])
+    b = np.stack([K.encrypt(int(x), s) for x in B])
+    a[1, :K.n] = 0  # every mod-switched a_i = 0 for this lane: all of its steps skipped
+    for kind in ("and", "or", "xor", "xnor", "nand", "nor"):
+        want = K.gate_batch(kind, a, b, O.FFT, 4)
+        assert np.array_equal(K.gate_batch_simd(kind, a, b, 3), want), kind
