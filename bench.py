@@ -380,7 +380,8 @@ CPU_LOCPIR_SAMPLES = {"cfg1": (1, None), "cfg3": (1, 8), "cfg4": (1, 8), "cfg5":
 
 
 def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
-    """The same loc_pir gate programs evaluated by the oracle port (FP64-FFT mode) level by
+    """The same loc_pir gate programs evaluated by the oracle port (FP64-FFT mode, blind
+    rotations lane-batched over SIMD vectors, bit-identical to the scalar port) level by
     level on all host threads (oracle.run_program), decrypted and checked against the
     plaintext answer.  cfg1 runs in full; cfg3/4/5 run on a box subsample and are
     extrapolated linearly in bootstrap units (SURVEY §8(d) "run cfg3/4/5 on a stated
@@ -415,7 +416,7 @@ def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
         pool[lay.svc.reshape(-1)] = enc_bits(sbits.reshape(-1))
         ops = W.program_ops(b, lay)
         t = time.perf_counter()
-        O.run_program(K, ops, pool, threads)
+        O.run_program(K, ops, pool, threads, simd=True)
         dt = time.perf_counter() - t
         got = np.array([sum(O.decrypt_bit(pool[lay.out[q, j]], K.lwe_key) << j for j in range(m))
                         for q in range(Qs)], np.uint64)

@@ -113,6 +113,8 @@ def lib():
         L.or_gate_batch_simd.argtypes = [C.POINTER(KeySet), C.c_int, u32p, u32p, u32p,
                                          C.c_uint64, C.c_int]
         L.or_simd_lanes.restype = C.c_int
+        L.or_gate_list_simd.argtypes = [C.POINTER(KeySet), C.POINTER(GateItem), C.c_uint64,
+                                        C.c_int]
         _lib = L
     return _lib
 
@@ -332,14 +334,16 @@ class TfheKeys:
 
 
 # gate-program kinds (include/locpir_b200.h) -> oracle kinds; NOT/COPY/CONST are free
-_PROG_BOOT = {0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5, 7: 7, 10: 10, 11: 11, 12: 12}
+_PROG_BOOT = {0: 0, 1: 1, 2: 2, 3: 3, 4: 4, 5: 5, 7: 7, 10: 10, 11: 11, 12: 12, 13: 13}
 _NOT, _COPY, _CONST = 6, 8, 9
 
 
-def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: int = FFT):
+def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: int = FFT,
+                simd: bool = False):
     """Evaluates a gate program (5-tuples or ctypes GateOps over pool slots, the layout of
     include/locpir_b200.h) on the oracle: bootstrapped gates level by level, each level
-    one threaded or_gate_list call; free gates in program order between levels.
+    one threaded or_gate_list call (simd=True: or_gate_list_simd, FFT mode, blind
+    rotations lane-batched, bit-identical); free gates in program order between levels.
     pool: [slots, n+1] uint32, updated in place.  Test / baseline infrastructure."""
     SLOT_NONE = 0xFFFFFFFF
     ops = [(o.kind, o.in0, o.in1, o.in2, o.out) if not isinstance(o, tuple) else o for o in ops]
@@ -365,7 +369,10 @@ def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: in
                                     base_ptr + b * row if b != SLOT_NONE else None,
                                     base_ptr + c * row if c != SLOT_NONE else None,
                                     base_ptr + o * row)
-            rc = lib().or_gate_list(C.byref(K.ks), items, len(boot), mode, threads)
+            if simd and mode == FFT:
+                rc = lib().or_gate_list_simd(C.byref(K.ks), items, len(boot), threads)
+            else:
+                rc = lib().or_gate_list(C.byref(K.ks), items, len(boot), mode, threads)
             if rc:
                 raise ValueError(f"oracle gate list failed: {rc}")
         for i in idx:

@@ -1332,3 +1332,121 @@ int or_gate_batch_simd(const or_keyset* ks, int kind, const uint32_t* a, const u
     free(tid);
     return rc;
 }
+
+/* A heterogeneous gate list (one level of a gate program) lane-batched like
+ * or_gate_batch_simd: every item's blind rotation(s) -- one per gate, two for a MUX --
+ * are gathered, rotated VL at a time, then key-switched per item exactly as or_gate does
+ * (bit-identical to or_gate_list(..., ORACLE_FFT, ...)). */
+typedef struct {
+    const or_keyset* ks;
+    const or_gate_item* items;
+    uint64_t lo, hi;
+    int rc;
+} list_simd_job;
+
+static void* list_simd_worker(void* arg)
+{
+    list_simd_job* jb = (list_simd_job*)arg;
+    const or_keyset* ks = jb->ks;
+    const uint32_t n = ks->p.n, N = ks->p.N;
+    const size_t w = n + 1;
+    const uint64_t cnt = jb->hi - jb->lo;
+    uint64_t nbr = 0;
+    for (uint64_t g = jb->lo; g < jb->hi; g++)
+        nbr += jb->items[g].kind == OR_GATE_MUX ? 2 : 1;
+    uint32_t* comb = (uint32_t*)malloc(sizeof(uint32_t) * w * (nbr + OR_LANES));
+    uint32_t* ext = (uint32_t*)malloc(sizeof(uint32_t) * (N + 1) * (nbr + OR_LANES));
+    uint64_t* first = (uint64_t*)malloc(sizeof(uint64_t) * (cnt + 1));
+    simd_ws* W = (simd_ws*)aligned_alloc(64, (sizeof(simd_ws) + 63) / 64 * 64);
+    uint64_t k = 0;
+    for (uint64_t g = jb->lo; g < jb->hi; g++) { /* linear forms (or_gate) */
+        const or_gate_item* it = &jb->items[g];
+        uint32_t* cb = comb + k * w;
+        first[g - jb->lo] = k;
+        switch (it->kind) {
+        case OR_GATE_AND: lin2(n, 0xE0000000u, 1, it->a, 1, it->b, cb); break;
+        case OR_GATE_OR: lin2(n, 0x20000000u, 1, it->a, 1, it->b, cb); break;
+        case OR_GATE_XOR: lin2(n, 0x40000000u, 2, it->a, 2, it->b, cb); break;
+        case OR_GATE_XNOR: lin2(n, 0xC0000000u, -2, it->a, -2, it->b, cb); break;
+        case OR_GATE_NAND: lin2(n, 0x20000000u, -1, it->a, -1, it->b, cb); break;
+        case OR_GATE_NOR: lin2(n, 0xE0000000u, -1, it->a, -1, it->b, cb); break;
+        case OR_GATE_ANDNY: lin2(n, 0xE0000000u, -1, it->a, 1, it->b, cb); break;
+        case OR_GATE_ORNY: lin2(n, 0x20000000u, -1, it->a, 1, it->b, cb); break;
+        case OR_GATE_MAJ:
+            lin2(n, 0u, 1, it->a, 1, it->b, cb);
+            for (uint32_t q = 0; q <= n; q++)
+                cb[q] += it->c[q];
+            break;
+        case OR_GATE_XOR3:
+            lin2(n, 0u, -2, it->a, -2, it->b, cb);
+            for (uint32_t q = 0; q <= n; q++)
+                cb[q] += (uint32_t)-2 * it->c[q];
+            break;
+        case OR_GATE_MUX:
+            lin2(n, 0xE0000000u, 1, it->a, 1, it->b, cb);
+            lin2(n, 0xE0000000u, -1, it->a, 1, it->c, cb + w);
+            k++;
+            break;
+        default: jb->rc = -1; goto out;
+        }
+        k++;
+    }
+    for (uint64_t g0 = 0; g0 < nbr; g0 += OR_LANES) { /* blind rotations, VL at a time */
+        const int lanes = (int)(nbr - g0 < OR_LANES ? nbr - g0 : OR_LANES);
+        const uint32_t* lw[OR_LANES];
+        uint32_t* eo[OR_LANES];
+        for (int L = 0; L < OR_LANES; L++) {
+            lw[L] = comb + (g0 + L) * w;
+            eo[L] = ext + (g0 + L) * (N + 1);
+        }
+        blind_rotate_extract_lanes(ks, lw, lanes, 0x20000000u, W, eo);
+    }
+    for (uint64_t g = jb->lo; g < jb->hi; g++) { /* key switches (or_gate) */
+        const or_gate_item* it = &jb->items[g];
+        uint32_t* e = ext + first[g - jb->lo] * (N + 1);
+        if (it->kind == OR_GATE_MUX) {
+            const uint32_t* e2 = e + (N + 1);
+            for (uint32_t q = 0; q <= N; q++)
+                e[q] += e2[q];
+            e[N] += 0x20000000u;
+        }
+        or_keyswitch(ks, e, it->out);
+    }
+out:
+    free(comb);
+    free(ext);
+    free(first);
+    free(W);
+    return NULL;
+}
+
+int or_gate_list_simd(const or_keyset* ks, const or_gate_item* items, uint64_t count, int threads)
+{
+    if (ks->p.N != OR_N)
+        return -1;
+    if (threads < 1)
+        threads = 1;
+    if ((uint64_t)threads > count)
+        threads = count ? (int)count : 1;
+    list_simd_job* jobs = (list_simd_job*)calloc(threads, sizeof(list_simd_job));
+    pthread_t* tid = (pthread_t*)calloc(threads, sizeof(pthread_t));
+    const uint64_t chunk = (count + threads - 1) / threads;
+    for (int t = 0; t < threads; t++) {
+        jobs[t].ks = ks;
+        jobs[t].items = items;
+        jobs[t].lo = (uint64_t)t * chunk < count ? (uint64_t)t * chunk : count;
+        jobs[t].hi = jobs[t].lo + chunk < count ? jobs[t].lo + chunk : count;
+    }
+    for (int t = 1; t < threads; t++)
+        pthread_create(&tid[t], NULL, list_simd_worker, &jobs[t]);
+    list_simd_worker(&jobs[0]);
+    int rc = jobs[0].rc;
+    for (int t = 1; t < threads; t++) {
+        pthread_join(tid[t], NULL);
+        if (jobs[t].rc)
+            rc = jobs[t].rc;
+    }
+    free(jobs);
+    free(tid);
+    return rc;
+}

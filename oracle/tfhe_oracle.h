@@ -186,6 +186,9 @@ typedef struct {
 } or_gate_item;
 int or_gate_list(const or_keyset* ks, const or_gate_item* items, uint64_t count, int mode,
                  int threads);
+/* The same list in FFT mode, blind rotations lane-batched (bit-identical; CPU baseline). */
+int or_gate_list_simd(const or_keyset* ks, const or_gate_item* items, uint64_t count,
+                      int threads);
 
 #ifdef __cplusplus
 }
