@@ -416,7 +416,7 @@ def cpu_locpir_baseline(threads=None, seed=KEY_SEED):
         pool[lay.svc.reshape(-1)] = enc_bits(sbits.reshape(-1))
         ops = W.program_ops(b, lay)
         t = time.perf_counter()
-        O.run_program(K, ops, pool, threads, simd=True)
+        O.run_program(K, ops, pool, threads, simd="auto")
         dt = time.perf_counter() - t
         got = np.array([sum(O.decrypt_bit(pool[lay.out[q, j]], K.lwe_key) << j for j in range(m))
                         for q in range(Qs)], np.uint64)

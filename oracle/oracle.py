@@ -339,11 +339,12 @@ _NOT, _COPY, _CONST = 6, 8, 9
 
 
 def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: int = FFT,
-                simd: bool = False):
+                simd=False):
     """Evaluates a gate program (5-tuples or ctypes GateOps over pool slots, the layout of
     include/locpir_b200.h) on the oracle: bootstrapped gates level by level, each level
     one threaded or_gate_list call (simd=True: or_gate_list_simd, FFT mode, blind
-    rotations lane-batched, bit-identical); free gates in program order between levels.
+    rotations lane-batched, bit-identical; simd="auto": per level, whichever of the two
+    is faster for its width); free gates in program order between levels.
     pool: [slots, n+1] uint32, updated in place.  Test / baseline infrastructure."""
     SLOT_NONE = 0xFFFFFFFF
     ops = [(o.kind, o.in0, o.in1, o.in2, o.out) if not isinstance(o, tuple) else o for o in ops]
@@ -369,8 +370,16 @@ def run_program(K: "TfheKeys", ops, pool: np.ndarray, threads: int = 1, mode: in
                                     base_ptr + b * row if b != SLOT_NONE else None,
                                     base_ptr + c * row if c != SLOT_NONE else None,
                                     base_ptr + o * row)
-            if simd and mode == FFT:
-                rc = lib().or_gate_list_simd(C.byref(K.ks), items, len(boot), threads)
+            # lane-batching pays once the level fills the lanes of the threads: a lane
+            # group of L rotations costs ~L/3 scalar gates with AVX-512 (measured ~3x per
+            # gate), so narrow levels (single queries) stay on the scalar path
+            nb = len(boot)
+            L = simd_lanes()
+            t_scalar = -(-nb // threads)
+            t_simd = -(-nb // (threads * L)) * L / 3.0
+            if mode == FFT and (simd is True or (simd == "auto" and t_simd < t_scalar)):
+                rc = lib().or_gate_list_simd(C.byref(K.ks), items, nb,
+                                             min(threads, -(-nb // L)))
             else:
                 rc = lib().or_gate_list(C.byref(K.ks), items, len(boot), mode, threads)
             if rc:
