@@ -715,3 +715,37 @@ def test_eager_and_level_batched_evaluation_give_identical_ciphertexts(dev):
         out = loc_pir(x, y, regions, eng, tree=True)
         outs.append(eng.samples(out.bits))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("name,R,kw", [("cfg3", 256, {}), ("cfg3", 256, {"folded": True}),
+                                       ("cfg4", 16, {}), ("cfg5", 64, {}),
+                                       ("cfg5", 64, {"maj": True})])
+def test_loc_pir_program_every_ciphertext_equals_oracle(dev, okeys128, name, R, kw):
+    """A whole LocPIR gate program on the B200 against the same program on the CPU oracle
+    -- cfg3 at its stated size (1 query x 256 boxes, 66,304 bootstraps), one query of cfg4
+    (16 boxes) and of cfg5 (64 boxes, encrypted boundaries, l = 32), reference circuit and
+    flagged modes (oracle.run_program): EVERY ciphertext of the pool -- inputs, each comparator, mask and
+    XOR-tree intermediate (a loc_pir program gives each its own slot) and the outputs -- is
+    bit-exact, and the outputs decrypt to the plaintext answer."""
+    import os
+    from oracle import oracle as O
+    from paper_2407_19871_b200 import workloads as W
+    sec, _, _, l, m, enc = W.CONFIGS[name]
+    p, keys, ctx = dev[128]
+    b = W.make_batch(1, R, l, m, seed=300 + R, encrypted_bounds=enc)
+    b.x[0] = (b.boxes[0, 0] + b.boxes[0, 1]) // 2
+    b.y[0] = (b.boxes[0, 2] + b.boxes[0, 3]) // 2
+    lay = W.PoolLayout(b)
+    ctx.pool_reserve(lay.total)
+    W.load_batch(ctx, keys, b, lay, seed=17)
+    before = ctx.d2h(0, lay.total)
+    ops = W.program_ops(b, lay, **kw)
+    prog = ctx.program(ops)
+    prog.launch()
+    gpu = ctx.d2h(0, lay.total)
+    prog.close()
+    assert np.array_equal(W.read_results(ctx, keys, b, lay), b.truth())
+    cpu = O.run_program(okeys128, ops, before.copy(), threads=os.cpu_count() or 1, simd="auto")
+    written = sorted({o.out for o in ops})
+    bad = [s for s in written if not np.array_equal(gpu[s], cpu[s])]
+    assert not bad, f"{len(bad)} of {len(written)} program ciphertexts differ, first slots {bad[:5]}"
