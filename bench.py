@@ -875,7 +875,11 @@ def run_b200(args):
             },
             "keyswitch": keyswitch_view(G, params, avg_ks_ms, ksk_bytes),
             "e2e": {"value": ws * G / e2e_s, "unit": "gates/s",
-                    "h2d_bytes_per_step": 2 * G * n1 * 4, "d2h_bytes_per_step": G * n1 * 4},
+                    "h2d_bytes_per_step": 2 * G * n1 * 4, "d2h_bytes_per_step": G * n1 * 4,
+                    "path": "locpir_b200_gate_batch_host on pinned host buffers: the input rows "
+                            "cross PCIe inside the blind rotation's prologue (zero-copy reads "
+                            "of the caller's buffers), the outputs are packed and copied back "
+                            "before the call returns"},
             "gpu_launches": args.steps * prog.kernels,
             "clocks": clk,
             "setup_s": setup_s,

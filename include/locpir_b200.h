@@ -175,7 +175,11 @@ int locpir_b200_counters_reset(locpir_b200_ctx* ctx);
 
 /* ---- end-to-end convenience: one batched gate on HOST buffers ------------------
  * out[i] = gate(a[i], b[i]) for i < count; a, b, out are [count][n+1] host arrays.
- * Includes the host->device and device->host copies. */
+ * Includes the host->device and device->host transfers.  When a and b are pinned
+ * (device-mapped, e.g. cudaHostAlloc) and count >= 256, the blind rotation reads the
+ * input rows over PCIe itself (zero-copy; LOCPIR_B200_ZEROCOPY=0 at context creation
+ * disables it); otherwise they are copied first.  Results are identical either way.
+ * The context's pool slots [0, count) (zero-copy) or [0, 3 count) (copy) are used. */
 int locpir_b200_gate_batch_host(locpir_b200_ctx* ctx, uint32_t kind, const uint32_t* a,
                                 const uint32_t* b, uint32_t* out, uint64_t count);
 

@@ -124,6 +124,10 @@ struct locpir_b200_ctx {
     // small levels (fewer bootstraps than SMs) take the latency kernels
     int small_levels = 1;
     int use_graphs = 1;   // LOCPIR_B200_GRAPH=0: programs launch without CUDA graphs
+    int zero_copy = 1;    // LOCPIR_B200_ZEROCOPY=0: gate_batch_host always copies its inputs
+    const uint32_t* ext_a = nullptr;  // zero-copy inputs of the running gate_batch_host
+    const uint32_t* ext_b = nullptr;
+    uint32_t ext_rows = 0;
     int l2_persist = 1;  // env LOCPIR_B200_L2PERSIST=0 disables
     // env LOCPIR_B200_POISON=<u32>: newly grown pool and scratch memory is filled with this
     // word instead of zeros / left undefined (self-check: results must not depend on it)
@@ -172,6 +176,9 @@ DevParams dparams(const locpir_b200_ctx* c)
     DevParams d = c->dp;
     d.pool_slots = c->pool_slots;
     d.scratch_slots = c->pool_N.n / c->dp.N_stride;
+    d.ext_a = c->ext_a;
+    d.ext_b = c->ext_b;
+    d.ext_rows = c->ext_rows;
     return d;
 }
 
@@ -603,6 +610,70 @@ void pool_copy(locpir_b200_ctx* c, uint64_t first, uint64_t count, const uint32_
     }
 }
 
+// Device address of a pinned, device-mapped host buffer (cudaHostAlloc / pinned torch
+// tensors under unified addressing), or nullptr for pageable memory.
+const uint32_t* mapped_host(const uint32_t* p)
+{
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? static_cast<const uint32_t*>(at.devicePointer) : nullptr;
+}
+
+// gate_batch_host on pinned inputs: the blind rotation's prologue reads each gate's two
+// input rows straight from the caller's buffers over PCIe (slots SLOT_EXT_A / _B), so no
+// host-to-device copy and no repack precede the first K1 wave; one level, so the items are
+// built directly (no planner).  Outputs land in pool slots [0, count) and are packed and
+// copied back as in the copy path.
+void gate_batch_zero_copy(locpir_b200_ctx* c, uint32_t kind, const GateForm& f,
+                          const uint32_t* da, const uint32_t* db, uint32_t* out, uint64_t count)
+{
+    need_keys(c);
+    check_owned(c, count);
+    if (c->pool_slots < count) {
+        int rc = locpir_b200_pool_reserve(c, count);
+        if (rc)
+            throw CudaError(c->err);
+    }
+    if (count > c->scratch_slots) {
+        grow_scratch(c, count);
+        c->scratch_slots = c->pool_N.n / c->dp.N_stride;
+    }
+    CK(cudaStreamSynchronize(c->stream));  // pinned staging may still feed an earlier copy
+    c->h_br.reserve(count + 1);
+    c->h_ks.reserve(count + 1);
+    for (uint64_t g = 0; g < count; g++) {
+        c->h_br.p[g] = {SLOT_EXT_A | (uint32_t)g, SLOT_EXT_B | (uint32_t)g, f.c0, f.c1, f.off,
+                        (uint32_t)g, SLOT_NONE, 0};
+        c->h_ks.p[g] = {(uint32_t)g, SLOT_NONE, 0u, (uint32_t)g};
+    }
+    c->d_br.reserve(count + 1, c->stream, false);
+    c->d_ks.reserve(count + 1, c->stream, false);
+    CK(cudaMemcpyAsync(c->d_br.p, c->h_br.p, count * sizeof(BrItem), cudaMemcpyHostToDevice,
+                       c->stream));
+    CK(cudaMemcpyAsync(c->d_ks.p, c->h_ks.p, count * sizeof(KsItem), cudaMemcpyHostToDevice,
+                       c->stream));
+    c->ext_a = da;
+    c->ext_b = db;
+    c->ext_rows = (uint32_t)count;
+    try {
+        launch_br(c, c->d_br.p, (uint32_t)count);
+    } catch (...) {
+        c->ext_a = c->ext_b = nullptr;
+        c->ext_rows = 0;
+        throw;
+    }
+    c->ext_a = c->ext_b = nullptr;
+    c->ext_rows = 0;
+    launch_ks(c, c->d_ks.p, (uint32_t)count);
+    static const int cidx[] = {0, 1, 2, 3, 6, -1, -1, 7, -1, -1, 0, 1};  // as Plan::counts
+    c->counters[cidx[kind]] += count;
+    c->counters[8] += count;
+    pool_copy(c, 0, count, nullptr, out, cudaMemcpyDeviceToHost, false);
+}
+
 // QUERY framing check in the order the reference's ByteReader consumes the bytes
 // (handle_query, protocol.hpp:401-407: read_word x2 + expect_done; codec.hpp:180-193;
 // bytes.hpp:66-130), throwing the reference's DecodeError messages as invalid_argument.
@@ -683,6 +754,8 @@ int locpir_b200_ctx_create(const locpir_b200_params* p, int device, void* stream
             c->small_levels = strcmp(sl, "0") != 0;
         if (const char* gr = getenv("LOCPIR_B200_GRAPH"))
             c->use_graphs = strcmp(gr, "0") != 0;
+        if (const char* zc = getenv("LOCPIR_B200_ZEROCOPY"))
+            c->zero_copy = strcmp(zc, "0") != 0;
         if (const char* po = getenv("LOCPIR_B200_POISON"); po && *po) {
             c->poison = (uint32_t)strtoul(po, nullptr, 0);
             c->poison_set = true;
@@ -1001,6 +1074,15 @@ int locpir_b200_gate_batch_host(locpir_b200_ctx* c, uint32_t kind, const uint32_
         if (count >= (1ull << 30) || (count && (!a || !b || !out)))
             throw std::invalid_argument("bad batch");
         CK(cudaSetDevice(c->device));
+        if (c->zero_copy && count >= 256 && count < (1ull << 29)) {
+            const uint32_t* da = mapped_host(a);
+            const uint32_t* db = mapped_host(b);
+            if (da && db) {
+                gate_batch_zero_copy(c, kind, f, da, db, out, count);
+                CK(cudaStreamSynchronize(c->stream));
+                return;
+            }
+        }
         if (c->pool_slots < 3 * count) {
             int rc = locpir_b200_pool_reserve(c, 3 * count);
             if (rc)

@@ -55,7 +55,14 @@ struct DevParams {
     uint32_t n_stride;  // padded n+1
     uint32_t N_stride;  // padded N+1
     uint64_t pool_slots, scratch_slots;  // current pool sizes (bounds for LPB_CHECKS)
+    // zero-copy inputs of one gate_batch_host call: packed [count][n+1] rows in pinned,
+    // device-mapped host memory, addressed by the slots SLOT_EXT_A / SLOT_EXT_B | row
+    const uint32_t* ext_a;
+    const uint32_t* ext_b;
+    uint32_t ext_rows;
 };
+constexpr uint32_t SLOT_EXT_A = 0x80000000u, SLOT_EXT_B = 0xC0000000u, SLOT_EXT_ROW = 0x3FFFFFFFu;
+
 
 // ---- self-check build (compute-sanitizer is closed on the GPU pool):
 //   LPB_CHECKS=1  device asserts on every pool / scratch / table index a kernel forms
@@ -73,6 +80,19 @@ struct DevParams {
 #else
 #define LPB_ASSERT(x) ((void)0)
 #endif
+// An input LWE row: a pool slot, or (gate_batch_host's zero-copy path) a row of the
+// caller's pinned host buffer read over PCIe by the blind rotation's prologue.
+__device__ __forceinline__ const uint32_t* lwe_row(const DevParams& dp, const uint32_t* pool_n,
+                                                   uint32_t slot)
+{
+    if (slot >= SLOT_EXT_A) {
+        LPB_ASSERT((slot & SLOT_EXT_ROW) < dp.ext_rows);
+        return ((slot & 0x40000000u) ? dp.ext_b : dp.ext_a) + (size_t)(slot & SLOT_EXT_ROW) * (dp.n + 1);
+    }
+    LPB_ASSERT(slot < dp.pool_slots);
+    return pool_n + (size_t)slot * dp.n_stride;
+}
+
 __constant__ uint32_t c_poison;  // LOCPIR_B200_POISON (checked build: shared memory poison)
 
 __global__ void k_fill(uint32_t* __restrict__ p, size_t words, uint32_t v)
@@ -240,9 +260,7 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
     const int t = threadIdx.x;
     const BrItem it = items[blockIdx.x];
     const uint32_t n = dp.n;
-    LPB_ASSERT(it.in0 < dp.pool_slots && it.out < dp.scratch_slots);
-    LPB_ASSERT((it.in1 == SLOT_NONE || it.in1 < dp.pool_slots) &&
-               (it.in2 == SLOT_NONE || it.in2 < dp.pool_slots) && n <= MAX_N);
+    LPB_ASSERT(it.out < dp.scratch_slots && n <= MAX_N);
 #if LPB_CHECKS
     lpb_poison_smem(acc, sizeof(acc));
     lpb_poison_smem(xbuf, sizeof(xbuf));
@@ -251,9 +269,9 @@ __global__ void __launch_bounds__(64, BR_MIN_BLOCKS)
 
     // ---- prologue: gate linear form (gate_engine.hpp:196-269) + mod switch to [0, 2N)
     {
-        const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
-        const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
-        const uint32_t* a2 = it.in2 != SLOT_NONE ? pool_n + (size_t)it.in2 * dp.n_stride : nullptr;
+        const uint32_t* a0 = lwe_row(dp, pool_n, it.in0);
+        const uint32_t* a1 = it.in1 != SLOT_NONE ? lwe_row(dp, pool_n, it.in1) : nullptr;
+        const uint32_t* a2 = it.in2 != SLOT_NONE ? lwe_row(dp, pool_n, it.in2) : nullptr;
         for (uint32_t i = t; i <= n; i += 64) {
             uint32_t v = (uint32_t)it.c0 * a0[i];
             if (a1)
@@ -772,12 +790,12 @@ __global__ void __launch_bounds__(128 * L, 1)
     const int g = threadIdx.x >> 6, t = threadIdx.x & 63;
     const BrItem it = items[blockIdx.x];
     const uint32_t n = dp.n;
-    LPB_ASSERT(it.in0 < dp.pool_slots && it.out < dp.scratch_slots && n <= MAX_N);
+    LPB_ASSERT(it.out < dp.scratch_slots && n <= MAX_N);
     lpb_poison_smem(smem_l, sizeof(LatSmem<L>));
     {
-        const uint32_t* a0 = pool_n + (size_t)it.in0 * dp.n_stride;
-        const uint32_t* a1 = it.in1 != SLOT_NONE ? pool_n + (size_t)it.in1 * dp.n_stride : nullptr;
-        const uint32_t* a2 = it.in2 != SLOT_NONE ? pool_n + (size_t)it.in2 * dp.n_stride : nullptr;
+        const uint32_t* a0 = lwe_row(dp, pool_n, it.in0);
+        const uint32_t* a1 = it.in1 != SLOT_NONE ? lwe_row(dp, pool_n, it.in1) : nullptr;
+        const uint32_t* a2 = it.in2 != SLOT_NONE ? lwe_row(dp, pool_n, it.in2) : nullptr;
         for (uint32_t i = threadIdx.x; i <= n; i += blockDim.x) {
             uint32_t v = (uint32_t)it.c0 * a0[i];
             if (a1)

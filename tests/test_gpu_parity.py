@@ -749,3 +749,30 @@ def test_loc_pir_program_every_ciphertext_equals_oracle(dev, okeys128, name, R, 
     written = sorted({o.out for o in ops})
     bad = [s for s in written if not np.array_equal(gpu[s], cpu[s])]
     assert not bad, f"{len(bad)} of {len(written)} program ciphertexts differ, first slots {bad[:5]}"
+
+
+@pytest.mark.parametrize("count", [256, 4097])
+def test_gate_batch_host_zero_copy_equals_copy_path(dev, okeys128, count):
+    """gate_batch_host on pinned host buffers reads the inputs over PCIe inside the blind
+    rotation (zero-copy); on pageable buffers it copies them first.  Both give the same
+    ciphertexts, equal to the oracle's."""
+    import torch
+    from paper_2407_19871_b200 import _abi
+    p, keys, ctx = dev[128]
+    rng = np.random.default_rng(count)
+    A = rng.integers(0, 2, count).astype(np.uint8)
+    B = rng.integers(0, 2, count).astype(np.uint8)
+    a = keys.encrypt_bits(A, 5)
+    b = keys.encrypt_bits(B, 6)
+    for kind, fn, name in ((_abi.NAND, lambda x, y: 1 - (x & y), "nand"),
+                           (_abi.XOR, lambda x, y: x ^ y, "xor")):
+        copied = ctx.gate_batch_host(kind, a, b)  # numpy: pageable -> copy path
+        a_h = torch.from_numpy(a.view(np.int32)).pin_memory()
+        b_h = torch.from_numpy(b.view(np.int32)).pin_memory()
+        o_h = torch.empty(a_h.shape, dtype=torch.int32).pin_memory()
+        ctx.gate_batch_host_ptr(kind, a_h.data_ptr(), b_h.data_ptr(), o_h.data_ptr(), count)
+        zc = o_h.numpy().view(np.uint32)
+        assert np.array_equal(zc, copied), name
+        assert np.array_equal(keys.decrypt_bits(zc), fn(A, B)), name
+        for g in (0, count - 1):
+            assert np.array_equal(zc[g], okeys128.gate(name, a[g], b[g])), name
