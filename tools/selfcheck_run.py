@@ -44,9 +44,17 @@ def main():
     G2 = 1280
     A2 = rng.integers(0, 2, G2).astype(np.uint8)
     B2 = rng.integers(0, 2, G2).astype(np.uint8)
-    out = ctx.gate_batch_host(_abi.NAND, keys.encrypt_bits(A2, 4), keys.encrypt_bits(B2, 5))
+    a2, b2 = keys.encrypt_bits(A2, 4), keys.encrypt_bits(B2, 5)
+    out = ctx.gate_batch_host(_abi.NAND, a2, b2)
     assert np.array_equal(keys.decrypt_bits(out), 1 - (A2 & B2))
     h.update(out.tobytes())
+    # the zero-copy path (pinned inputs read over PCIe by the blind rotation's prologue)
+    import torch
+    ah = torch.from_numpy(a2.view(np.int32)).pin_memory()
+    bh = torch.from_numpy(b2.view(np.int32)).pin_memory()
+    oh = torch.empty(ah.shape, dtype=torch.int32).pin_memory()
+    ctx.gate_batch_host_ptr(_abi.NAND, ah.data_ptr(), bh.data_ptr(), oh.data_ptr(), G2)
+    assert np.array_equal(oh.numpy().view(np.uint32), out)
     # a small loc_pir batch (comparator chains, masks, XOR tree; K1l/K2s levels and K3)
     bt = W.make_batch(3, 4, 8, 3, seed=5)
     bt.x[0] = (bt.boxes[0, 0] + bt.boxes[0, 1]) // 2
