@@ -29,6 +29,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+T_PROCESS = time.perf_counter()  # the wall-budget guard of the stated-size LocPIR runs counts from here
 sys.path.insert(0, ROOT)
 
 GATES_PER_GPU = 65536
@@ -439,6 +440,7 @@ LOCPIR_SAMPLES = {  # name: queries timed per rank for the flagged modes and --l
 # queries per program at the stated sizes (each program's scratch: ~19.6 MB per cfg4 query,
 # ~154 MB per cfg5 query; every level still spans >= 10 waves of the 148 SMs)
 LOCPIR_CHUNK = {"cfg4": 512, "cfg5": 128}
+WALL_RESERVE_S = 75.0  # what follows the stated-size runs: flagged samples, batcher, CPU baselines
 
 
 def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
@@ -479,6 +481,19 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
             # the reference circuit runs the config at its stated size (all Qfull queries
             # inside the timed region); flagged modes run a labelled per-GPU sample
             full = suffix == "" and args.locpir == "full"
+            budget_note = None
+            if full and Qfull > LOCPIR_SAMPLES[name]:
+                # wall-budget guard: a stated-size run is one timed launch of known length
+                # (its bootstraps / the cfg2 gate rate just measured; cfg5 = 26.4 M ~ 250 s).
+                # If it would end past --wall-budget (a slower or power-capped box), run the
+                # labelled sample instead of overrunning the caller's limit.  The elapsed
+                # time is the max over ranks, so every rank takes the same branch.
+                est_s = 1.08 * Qfull * R * (12 * l + 2 * m + 3) / ws / max(1.0, args.gate_rate)
+                elapsed = max_over_ranks(time.perf_counter() - T_PROCESS)
+                if elapsed + est_s + WALL_RESERVE_S > args.wall_budget:
+                    full = False
+                    budget_note = (f"stated size skipped by --wall-budget {args.wall_budget:.0f} s: "
+                                   f"{elapsed:.0f} s elapsed, run predicted {est_s:.0f} s")
             Q = Qfull if full else min(Qfull, LOCPIR_SAMPLES[name])
             # cfg1 replicas (independent queries per GPU); cfg3 boxes sharded
             # (partial XOR roots all-gathered, rank-0 combine level); cfg4/cfg5 queries
@@ -562,6 +577,8 @@ def run_locpir_suite(args, ctx128, keys128, ws, rank, local, max_over_ranks):
                                                            "once the GPU is saturated)",
                 "roofline": locpir_roofline(sec, units / Qb, qtot / (ms / 1e3), ws, fp64_peak),
             }
+            if budget_note:
+                out[name + suffix]["wall_budget"] = budget_note
             run.close()
     if not args.locpir_configs or "cfg4" in args.locpir_configs.split(","):
         out["cfg4_server"] = run_server_sample(ctx128, keys128, ws, max_over_ranks)
@@ -843,6 +860,7 @@ def run_b200(args):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     e2e_ok = bool(np.array_equal(keys.decrypt_bits(o_h.numpy().view(np.uint32)), 1 - (A & B)))
 
+    args.gate_rate = value / ws  # per-GPU bootstraps/s, for the wall-budget guard
     locpir_results = None if args.no_locpir else run_locpir_suite(args, ctx, keys, ws, rank,
                                                                    local, max_over_ranks)
     if rank == 0:
@@ -996,6 +1014,10 @@ def main():
     ap.add_argument("--locpir", default="full", choices=["full", "sample"],
                     help="full: cfg4/cfg5 reference circuits at their stated sizes (default); "
                          "sample: LOCPIR_SAMPLES queries per GPU (quick runs)")
+    ap.add_argument("--wall-budget", type=float, default=720.0,
+                    help="seconds of wall time the whole run may take: a stated-size LocPIR run "
+                         "predicted to end later falls back to its labelled sample (a default "
+                         "run takes ~8 min on a B200 at full clocks)")
     ap.add_argument("--gates", type=int, default=GATES_PER_GPU,
                     help="gates per GPU (default: the cfg2 size; smaller only for profiling)")
     ap.add_argument("--locpir-configs", default="",
